@@ -1,0 +1,205 @@
+/*
+ * manigraph_b200.h -- C ABI of the B200-native (A, B) formation + LOBPCG path.
+ *
+ * Drop-in boundary for the reference package `manigraph` (pure Python; its
+ * public API is re-exported at /root/reference/pkg/src/manigraph/__init__.py
+ * :23-66).  Every entry point below replaces one reference function; the
+ * citation names the function and file:line it replaces.  The reference has
+ * no FFI of its own, so the binding a maintainer would add is a ctypes shim
+ * (INTEGRATION.md shows it; paper_2112_07862_b200/_native.py is that shim).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Unless a parameter says "host", array
+ *    pointers are CUDA DEVICE pointers on the context's device.
+ *  - CSR matrices: indptr int64[n+1], indices int64[nnz] (sorted, unique per
+ *    row), data double[nnz]  (the reference dtypes, sparse.py:25-27).
+ *  - Block vectors are row-major n x k double arrays (numpy C order, the
+ *    layout of the reference's `eigenvectors` arrays).
+ *  - Work is stream-ordered on the context's stream; every call returns after
+ *    its results are complete (blocking from the caller's view, like the
+ *    reference's synchronous Python calls).
+ *  - Outputs of data-dependent size use a two-phase protocol: a *_count call
+ *    fills indptr and returns nnz on the host, the caller allocates, then the
+ *    *_fill call writes indices/data.
+ *  - Return value: an mg_status code.  mg_last_error() returns a thread-local
+ *    message for the last failing call on this thread.  Codes map to the
+ *    reference exceptions (errors.py:6-45): MG_ERR_INPUT -> InputError,
+ *    MG_ERR_DISCONNECTED -> DisconnectedGraphError, MG_ERR_NOT_CONVERGED ->
+ *    ConvergenceError (outputs are still filled, best effort).
+ */
+#ifndef MANIGRAPH_B200_H
+#define MANIGRAPH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum mg_status {
+  MG_OK = 0,
+  MG_ERR_INPUT = 1,
+  MG_ERR_DISCONNECTED = 2,
+  MG_ERR_NOT_CONVERGED = 3,
+  MG_ERR_CUDA = 4,
+  MG_ERR_NCCL = 5,
+  MG_ERR_NOMEM = 6,
+  MG_ERR_INTERNAL = 7
+} mg_status;
+
+typedef struct mg_ctx mg_ctx;
+
+/* ---- library / context ------------------------------------------------- */
+int mg_version(void);                                  /* ABI version */
+const char *mg_last_error(void);                       /* thread-local */
+int mg_device_count(int *count /* host */);
+/* stream: a cudaStream_t or NULL for a library-owned stream */
+int mg_ctx_create(int device, void *stream, mg_ctx **out);
+int mg_ctx_destroy(mg_ctx *ctx);
+int mg_ctx_set_stream(mg_ctx *ctx, void *stream);
+/* Number of native kernel launches issued through this context so far. */
+int mg_ctx_launch_count(mg_ctx *ctx, int64_t *count /* host */);
+
+/* ---- graph-level pieces -------------------------------------------------- */
+/* Graph.connected_components (graph.py:107-123): count + labels numbered by
+ * each component's smallest node id (the reference's DFS scan order). */
+int mg_components(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                  int64_t *labels /* device n, may be NULL */, int64_t *count /* host */);
+
+/* laplacian (graph.py:321-346) incl. degrees (graph.py:93-96).  Output nnz is
+ * always nnz(graph) + n; out_indptr n+1. */
+int mg_laplacian(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                 const double *weights, int64_t *out_indptr, int64_t *out_indices,
+                 double *out_data);
+
+/* two_hop_sets (operators.py:88-108): pattern(adj@adj) - diag - pattern(adj). */
+int mg_two_hop_count(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                     int64_t *t_indptr /* n+1 */, int64_t *t_nnz /* host */);
+int mg_two_hop_fill(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                    const int64_t *t_indptr, int64_t *t_indices);
+
+/* two_hop_laplacian (operators.py:111-135). */
+int mg_two_hop_laplacian_count(mg_ctx *ctx, int64_t n, const int64_t *t_indptr,
+                               int64_t *q_indptr /* n+1 */, int64_t *q_nnz /* host */);
+int mg_two_hop_laplacian_fill(mg_ctx *ctx, int64_t n, const int64_t *t_indptr,
+                              const int64_t *t_indices, int literal_diagonal,
+                              const int64_t *q_indptr, int64_t *q_indices, double *q_data);
+
+/* SparseSymMatrix.check_symmetric (sparse.py:100-105): *is_symmetric = 0/1. */
+int mg_check_symmetric(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                       const double *data, double rtol, int *is_symmetric /* host */);
+
+/* repulsion_weight (operators.py:159-176); returns MG_ERR_INPUT for eps < 0. */
+int mg_repulsion_weight(mg_ctx *ctx, int64_t n, const int64_t *q_indptr,
+                        const int64_t *q_indices, const double *q_data, double epsilon,
+                        double *mu /* host */);
+
+/* assemble_operator (operators.py:179-186): (L - mu*Q) + eps*I with exact-zero
+ * dropping and the reference's separate roundings. */
+int mg_assemble_count(mg_ctx *ctx, int64_t n, const int64_t *l_indptr, const int64_t *l_indices,
+                      const double *l_data, const int64_t *q_indptr, const int64_t *q_indices,
+                      const double *q_data, double mu, double epsilon,
+                      int64_t *a_indptr /* n+1 */, int64_t *a_nnz /* host */);
+int mg_assemble_fill(mg_ctx *ctx, int64_t n, const int64_t *l_indptr, const int64_t *l_indices,
+                     const double *l_data, const int64_t *q_indptr, const int64_t *q_indices,
+                     const double *q_data, double mu, double epsilon, const int64_t *a_indptr,
+                     int64_t *a_indices, double *a_data);
+
+/* degree_balancing (operators.py:205-219) + balance_radii (189-202) +
+ * SparseSymMatrix.gershgorin (sparse.py:84-94).  On MG_ERR_DISCONNECTED
+ * *isolated_node holds the first row with radius <= 0. */
+int mg_degree_balancing(mg_ctx *ctx, int64_t n, const int64_t *a_indptr,
+                        const int64_t *a_indices, const double *a_data, double *b /* device n */,
+                        double *generalized_degree /* host */, int64_t *isolated_node /* host */);
+
+/* OperatorPair.diagnostics (operators.py:76-85): min disc left end + row. */
+int mg_disc_left_min(mg_ctx *ctx, int64_t n, const int64_t *a_indptr, const int64_t *a_indices,
+                     const double *a_data, double *min_left /* host */,
+                     int64_t *binding_row /* host */);
+
+/* ---- eigensolver ----------------------------------------------------------- */
+typedef struct mg_solver_cfg {
+  int32_t k;               /* block size (SolverConfig.k, eigensolver.py:32-48) */
+  int32_t max_iter;
+  double tol;
+  int32_t preconditioner;  /* 0 none, 1 jacobi */
+  int32_t precision;       /* 0 fp64, 1 fp32 vectors with fp64 Gram/Rayleigh-Ritz */
+  int32_t reorder;         /* 1: locality reordering of rows inside the solve */
+  int32_t reserved;        /* mg_embed only: 1 = return all K+1 pairs in P/eigenvalues */
+} mg_solver_cfg;
+
+typedef struct mg_solver_out {
+  double *eigenvalues;      /* host k */
+  double *residual_norms;   /* host k */
+  int32_t *converged;       /* host k */
+  double *history;          /* host, capacity history_cap (ritz_sum_history) */
+  int32_t history_cap;
+  int32_t iterations;       /* out */
+  int32_t history_len;      /* out */
+  int32_t normals_used;     /* out: entries consumed from the normal stream */
+} mg_solver_out;
+
+/* lobpcg_smallest (eigensolver.py:156-283).  `normals` is the seeded standard
+ * normal stream (numpy PCG64(seed).standard_normal order): the initial block
+ * is normals[0 : n*k] read as n x k row-major, refills continue the stream
+ * (eigensolver.py:177-178, 189).  `deflate` (device n, or NULL) is one vector
+ * projected out in the B inner product (eigensolver.py:179-184, 239-241).
+ * eigenvectors: device n x k row-major.  Returns MG_OK even when not all
+ * pairs converged (check out->converged), like the reference. */
+int mg_lobpcg(mg_ctx *ctx, int64_t n, const int64_t *a_indptr, const int64_t *a_indices,
+              const double *a_data, const double *b, const mg_solver_cfg *cfg,
+              const double *normals, int64_t n_normals, const double *deflate,
+              double *eigenvectors, mg_solver_out *out);
+
+/* smallest_above_null (eigensolver.py:431-460) as used by identity_shift
+ * (operators.py:138-156): smallest eigenvalue of Q above tau = 1e-8 tr(Q)/n,
+ * dense for n <= 512, else deflated LOBPCG (k = 8 doubling to 64, tol 1e-6,
+ * 60 iterations).  Includes check_symmetric (MG_ERR_INPUT if asymmetric). */
+int mg_identity_shift(mg_ctx *ctx, int64_t n, const int64_t *q_indptr,
+                      const int64_t *q_indices, const double *q_data,
+                      const double *normals, int64_t n_normals, int32_t precision,
+                      double *epsilon /* host */);
+
+/* smallest_above_null (eigensolver.py:431-460) with explicit tau/tol/max_iter
+ * (fiedler_value, eigensolver.py:463-468, uses tol 1e-8 / 500).  No symmetry check. */
+int mg_smallest_above_null(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                           const double *data, double tau, double tol, int32_t max_iter,
+                           const double *normals, int64_t n_normals, int32_t precision,
+                           double *value /* host */);
+
+/* SparseSymMatrix.matmat (sparse.py:67-68): Y = A X, X/Y device n x k row-major. */
+int mg_spmm(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+            const double *data, const double *X, int32_t k, double *Y);
+
+/* ---- end-to-end ------------------------------------------------------------ */
+typedef struct mg_embed_diag {
+  double mu, epsilon, min_disc_left_end, dropped_eigenvalue, generalized_degree;
+  int64_t binding_row, q_nnz, a_nnz, t_nnz, n_components;
+  int32_t iterations, eps_iterations;
+  double seconds_setup, seconds_eps, seconds_solve;
+} mg_embed_diag;
+
+/* embed (embedding.py:77-103): components check, build_operator_pair,
+ * K+1-pair LOBPCG, drop the first pair.  P: device n x K row-major;
+ * eigenvalues host K; b device n.  `normals` as in mg_lobpcg (needs
+ * n * max(K+1, 8) entries).  check_connected = 0 bypasses the component test
+ * (SURVEY F6, config 4).  Returns MG_ERR_NOT_CONVERGED (outputs filled) when
+ * require_convergence and some pair is unconverged. */
+int mg_embed(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+             const double *weights, int32_t K, const mg_solver_cfg *cfg,
+             int32_t literal_diagonal, int32_t require_convergence, int32_t check_connected,
+             const double *normals, int64_t n_normals, double *P, double *b,
+             mg_solver_out *out, mg_embed_diag *diag);
+
+/* Same as mg_embed with HOST input/output arrays (library allocates device
+ * memory; host<->device copies happen inside). */
+int mg_embed_host(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                  const double *weights, int32_t K, const mg_solver_cfg *cfg,
+                  int32_t literal_diagonal, int32_t require_convergence,
+                  int32_t check_connected, const double *normals, int64_t n_normals,
+                  double *P, double *b, mg_solver_out *out, mg_embed_diag *diag);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MANIGRAPH_B200_H */

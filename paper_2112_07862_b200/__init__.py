@@ -1,0 +1,44 @@
+"""B200-native (A, B) formation + LOBPCG for manifold-graph embedding (arXiv 2112.07862).
+
+Drop-in for the hot path of the reference package ``manigraph``: the names
+below mirror ``manigraph/__init__.py:23-66`` for the embedding path.  The
+arithmetic runs in hand-written sm_100a kernels (``csrc/``) behind the C ABI
+``include/manigraph_b200.h``; there is no CPU fallback.
+"""
+
+__version__ = "0.1.0"
+
+from .core import (  # noqa: F401
+    DiagonalScaling,
+    EigenResult,
+    Embedding,
+    Graph,
+    OperatorPair,
+    SolverConfig,
+    SparseSymMatrix,
+    TwoHopSets,
+    assemble_operator,
+    build_operator_pair,
+    connected_components,
+    degree_balancing,
+    embed,
+    fiedler_value,
+    identity_shift,
+    laplacian,
+    laplacian_eigenmaps,
+    lobpcg_smallest,
+    repulsion_weight,
+    require_converged,
+    smallest_above_null,
+    spmm,
+    two_hop_laplacian,
+    two_hop_sets,
+)
+from .errors import (  # noqa: F401
+    ConvergenceError,
+    DisconnectedGraphError,
+    InputError,
+    ManigraphError,
+    ParseError,
+)
+from ._native import NativeUnavailable  # noqa: F401

@@ -1,0 +1,149 @@
+"""ctypes binding of the C ABI in include/manigraph_b200.h (libmgb200.so).
+
+This is the binding a maintainer would add to the reference package (which
+has no FFI of its own): plain pointers, sizes and status codes.  The library
+is loaded from ``paper_2112_07862_b200/_native/libmgb200.so`` (built in-tree
+by ``__graft_entry__.build()``); there is no fallback -- if the library or a
+CUDA device is missing, every compute call raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_native", "libmgb200.so")
+
+MG_OK, MG_ERR_INPUT, MG_ERR_DISCONNECTED, MG_ERR_NOT_CONVERGED = 0, 1, 2, 3
+MG_ERR_CUDA, MG_ERR_NCCL, MG_ERR_NOMEM, MG_ERR_INTERNAL = 4, 5, 6, 7
+
+i64 = C.c_int64
+i32 = C.c_int32
+f64 = C.c_double
+vp = C.c_void_p
+P_i64 = C.POINTER(C.c_int64)
+P_i32 = C.POINTER(C.c_int32)
+P_f64 = C.POINTER(C.c_double)
+P_int = C.POINTER(C.c_int)
+
+
+class SolverCfg(C.Structure):
+    _fields_ = [("k", i32), ("max_iter", i32), ("tol", f64), ("preconditioner", i32),
+                ("precision", i32), ("reorder", i32), ("reserved", i32)]
+
+
+class SolverOut(C.Structure):
+    _fields_ = [("eigenvalues", P_f64), ("residual_norms", P_f64), ("converged", P_i32),
+                ("history", P_f64), ("history_cap", i32), ("iterations", i32),
+                ("history_len", i32), ("normals_used", i32)]
+
+
+class EmbedDiag(C.Structure):
+    _fields_ = [("mu", f64), ("epsilon", f64), ("min_disc_left_end", f64),
+                ("dropped_eigenvalue", f64), ("generalized_degree", f64),
+                ("binding_row", i64), ("q_nnz", i64), ("a_nnz", i64), ("t_nnz", i64),
+                ("n_components", i64), ("iterations", i32), ("eps_iterations", i32),
+                ("seconds_setup", f64), ("seconds_eps", f64), ("seconds_solve", f64)]
+
+
+# name -> argtypes (restype is always c_int status, except mg_last_error / mg_version)
+SIGNATURES = {
+    "mg_device_count": [P_int],
+    "mg_ctx_create": [C.c_int, vp, C.POINTER(vp)],
+    "mg_ctx_destroy": [vp],
+    "mg_ctx_set_stream": [vp, vp],
+    "mg_ctx_launch_count": [vp, P_i64],
+    "mg_components": [vp, i64, vp, vp, vp, P_i64],
+    "mg_laplacian": [vp, i64, vp, vp, vp, vp, vp, vp],
+    "mg_two_hop_count": [vp, i64, vp, vp, vp, P_i64],
+    "mg_two_hop_fill": [vp, i64, vp, vp, vp, vp],
+    "mg_two_hop_laplacian_count": [vp, i64, vp, vp, P_i64],
+    "mg_two_hop_laplacian_fill": [vp, i64, vp, vp, C.c_int, vp, vp, vp],
+    "mg_check_symmetric": [vp, i64, vp, vp, vp, f64, P_int],
+    "mg_repulsion_weight": [vp, i64, vp, vp, vp, f64, P_f64],
+    "mg_assemble_count": [vp, i64, vp, vp, vp, vp, vp, vp, f64, f64, vp, P_i64],
+    "mg_assemble_fill": [vp, i64, vp, vp, vp, vp, vp, vp, f64, f64, vp, vp, vp],
+    "mg_degree_balancing": [vp, i64, vp, vp, vp, vp, P_f64, P_i64],
+    "mg_disc_left_min": [vp, i64, vp, vp, vp, P_f64, P_i64],
+    "mg_lobpcg": [vp, i64, vp, vp, vp, vp, C.POINTER(SolverCfg), vp, i64, vp, vp,
+                  C.POINTER(SolverOut)],
+    "mg_identity_shift": [vp, i64, vp, vp, vp, vp, i64, i32, P_f64],
+    "mg_smallest_above_null": [vp, i64, vp, vp, vp, f64, f64, i32, vp, i64, i32, P_f64],
+    "mg_spmm": [vp, i64, vp, vp, vp, vp, i32, vp],
+    "mg_embed": [vp, i64, vp, vp, vp, i32, C.POINTER(SolverCfg), i32, i32, i32, vp, i64, vp, vp,
+                 C.POINTER(SolverOut), C.POINTER(EmbedDiag)],
+    "mg_embed_host": [vp, i64, vp, vp, vp, i32, C.POINTER(SolverCfg), i32, i32, i32, vp, i64,
+                      vp, vp, C.POINTER(SolverOut), C.POINTER(EmbedDiag)],
+}
+
+
+class NativeUnavailable(RuntimeError):
+    """The sm_100a library or a CUDA device is missing (there is no CPU path)."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code, message):
+        super().__init__(message)
+        self.code = code
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str = LIB_PATH):
+    """Load and type the native library (no CUDA calls are made)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"native library not built: {path} (run __graft_entry__.build())")
+        lib = C.CDLL(path)
+        for name, args in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        lib.mg_last_error.restype = C.c_char_p
+        lib.mg_last_error.argtypes = []
+        lib.mg_version.restype = C.c_int
+        lib.mg_version.argtypes = []
+        _lib = lib
+        return lib
+
+
+def call(name, *args):
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != MG_OK:
+        msg = lib.mg_last_error().decode("utf-8", "replace")
+        raise NativeError(rc, msg)
+    return rc
+
+
+_ctx = {}
+
+
+def context(device: int = 0):
+    """Process-wide library context on ``device`` (library-owned stream)."""
+    if device in _ctx:
+        return _ctx[device]
+    lib = load()
+    n = C.c_int(0)
+    rc = lib.mg_device_count(C.byref(n))
+    if rc != MG_OK or n.value <= device:
+        raise NativeUnavailable("no CUDA device available for the sm_100a path: "
+                                + lib.mg_last_error().decode())
+    h = vp()
+    call("mg_ctx_create", device, None, C.byref(h))
+    _ctx[device] = h
+    return h
+
+
+def launch_count(device: int = 0) -> int:
+    v = C.c_int64(0)
+    call("mg_ctx_launch_count", context(device), C.byref(v))
+    return int(v.value)

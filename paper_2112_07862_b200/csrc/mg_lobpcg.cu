@@ -1,0 +1,1188 @@
+// B200 LOBPCG for the generalized problem (A, diag(b)) -- device side of
+// lobpcg_smallest (/root/reference/pkg/src/manigraph/eigensolver.py:156-283).
+//
+// Layout (row-major, one row per graph node, HBM-resident for the whole
+// solve):  S = [ X | P | W | y ]  and  AS = A*S  with column regions padded to
+// mp = roundup(m, 16B/sizeof(T)):  X at [0,mp), P at [mp,2mp), W at [2mp,3mp),
+// deflation vector y at 3mp.  One SpMM per iteration (A*W); X/P images are
+// carried (eigensolver.py:243-246).
+//
+// Per iteration (reference line numbers in brackets):
+//   resid      R = AX - (bX)Theta, norms, W = dinv*R           [217-222, 235-238]
+//   (host)     convergence test / verify branch / active set   [225-236]
+//   deflate    W -= y (y'BW)/(y'By)                            [239-241, 92-99]
+//   spmm       AW = A W                                        [243]
+//   pass1..3   two block projections of [W P] against X        [118-129]
+//   chol       B-Gram Cholesky with the 1e-12 drop rule        [133-152]
+//   pass4      apply R^-1, B-Gram of the result, A-Gram        [251]
+//   rr         CholQR2 correction + Rayleigh-Ritz (Jacobi)     [252-254]
+//   pass5      X = S Y, P = S[:,k:] Y[k:], and A-images        [255-259]
+// Full re-orthonormalisation (no trusted prefix) every 32 iterations [249].
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "mg_block.cuh"
+#include "mg_graph.cuh"
+#include "mg_small.cuh"
+
+namespace mg {
+
+static constexpr int kTR = 32;           // rows per tile pass tile
+static constexpr int kPassThreads = 256;
+static constexpr int kGT = 3;            // Gram register tiles per thread
+static constexpr int kCtrlThreads = 512;
+static constexpr int kMaxL = 256;
+
+// ------------------------------------------------------- CSR conversion ---
+template <typename T>
+__global__ void k_csr_convert(int64_t nnz, const int64_t *__restrict__ idx,
+                              const double *__restrict__ val, int *__restrict__ oidx,
+                              T *__restrict__ oval) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    oidx[e] = (int)idx[e];
+    oval[e] = (T)val[e];
+  }
+}
+
+template <typename T>
+void make_solver_csr(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *idx,
+                     const double *val, OwnedCSR<T> &out, int64_t nnz_hint) {
+  int64_t nnz = nnz_hint;
+  if (nnz < 0) d2h_sync(ctx, &nnz, ptr + n, sizeof(int64_t));
+  out.ptr.alloc(ctx, n + 1);
+  MG_CUDA(cudaMemcpyAsync(out.ptr.p, ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  out.idx.alloc(ctx, nnz > 0 ? nnz : 1);
+  out.val.alloc(ctx, nnz > 0 ? nnz : 1);
+  if (nnz > 0) {
+    k_csr_convert<T><<<grid_for(nnz, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        nnz, idx, val, out.idx.p, out.val.p);
+    MG_CHECK_LAUNCH(ctx);
+  }
+  out.view.n = n;
+  out.view.nnz = nnz;
+  out.view.ptr = out.ptr.p;
+  out.view.idx = out.idx.p;
+  out.view.val = out.val.p;
+}
+
+// ------------------------------------------------------------------ SpMM ---
+// Sub-warp of L lanes per CSR row; lane l owns columns [l*VN, l*VN+VN) of the
+// row-major block, so each nonzero costs one 16-byte coalesced load of the
+// neighbour's row segment.  Four nonzeros in flight per lane.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_spmm(int64_t n, const int64_t *__restrict__ ptr, const int *__restrict__ idx,
+           const T *__restrict__ val, const T *__restrict__ X, int ldx, T *__restrict__ Y, int ldy,
+           int L) {
+  using V = typename VecT<T>::V;
+  constexpr int VN = VecT<T>::N;
+  int lane = threadIdx.x & 31;
+  int G = 32 / L;
+  int g = lane / L, gl = lane - g * L;
+  if (g >= G) return;
+  int64_t per_block = (int64_t)(blockDim.x >> 5) * G;
+  int64_t stride = (int64_t)gridDim.x * per_block;
+  for (int64_t row = blockIdx.x * per_block + (threadIdx.x >> 5) * G + g; row < n; row += stride) {
+    int64_t s = ptr[row], e = ptr[row + 1];
+    T acc[VN];
+#pragma unroll
+    for (int q = 0; q < VN; ++q) acc[q] = T(0);
+    int64_t k = s;
+    for (; k + 4 <= e; k += 4) {
+      int j0 = __ldg(idx + k), j1 = __ldg(idx + k + 1), j2 = __ldg(idx + k + 2),
+          j3 = __ldg(idx + k + 3);
+      T v0 = __ldg(val + k), v1 = __ldg(val + k + 1), v2 = __ldg(val + k + 2),
+        v3 = __ldg(val + k + 3);
+      V x0 = __ldg(reinterpret_cast<const V *>(X + (int64_t)j0 * ldx) + gl);
+      V x1 = __ldg(reinterpret_cast<const V *>(X + (int64_t)j1 * ldx) + gl);
+      V x2 = __ldg(reinterpret_cast<const V *>(X + (int64_t)j2 * ldx) + gl);
+      V x3 = __ldg(reinterpret_cast<const V *>(X + (int64_t)j3 * ldx) + gl);
+      const T *p0 = reinterpret_cast<const T *>(&x0), *p1 = reinterpret_cast<const T *>(&x1),
+              *p2 = reinterpret_cast<const T *>(&x2), *p3 = reinterpret_cast<const T *>(&x3);
+#pragma unroll
+      for (int q = 0; q < VN; ++q) {
+        acc[q] += v0 * p0[q];
+        acc[q] += v1 * p1[q];
+        acc[q] += v2 * p2[q];
+        acc[q] += v3 * p3[q];
+      }
+    }
+    for (; k < e; ++k) {
+      int j0 = __ldg(idx + k);
+      T v0 = __ldg(val + k);
+      V x0 = __ldg(reinterpret_cast<const V *>(X + (int64_t)j0 * ldx) + gl);
+      const T *p0 = reinterpret_cast<const T *>(&x0);
+#pragma unroll
+      for (int q = 0; q < VN; ++q) acc[q] += v0 * p0[q];
+    }
+    V out;
+    T *po = reinterpret_cast<T *>(&out);
+#pragma unroll
+    for (int q = 0; q < VN; ++q) po[q] = acc[q];
+    reinterpret_cast<V *>(Y + row * ldy)[gl] = out;
+  }
+}
+
+template <typename T>
+void spmm(mg_ctx *ctx, const DevCSR<T> &A, const T *X, int ldx, T *Y, int ldy, int w) {
+  constexpr int VN = VecT<T>::N;
+  int L = w / VN;
+  require(L >= 1 && L <= 32 && w % VN == 0, MG_ERR_INTERNAL, "spmm width");
+  int G = 32 / L;
+  int64_t rows_per_block = 8 * G;
+  int grid = grid_for(A.n, (int)rows_per_block, ctx->num_sms * 64);
+  k_spmm<T><<<grid, 256, 0, ctx->stream>>>(A.n, A.ptr, A.idx, A.val, X, ldx, Y, ldy, L);
+  MG_CHECK_LAUNCH(ctx);
+}
+
+// -------------------------------------------------------- column kernels ---
+// Residual block R = AX - (b X) Theta (eigensolver.py:218), column sums of
+// R^2 and X^2 (219-220), W = dinv * R (235-238) written into region W.
+template <typename T>
+__global__ void k_resid(int64_t n, const T *__restrict__ S, const T *__restrict__ AS, int ld,
+                        int m, int mp, int wcol, const double *__restrict__ theta,
+                        const T *__restrict__ b, const T *__restrict__ prec, T *__restrict__ Wd,
+                        double *__restrict__ part) {
+  extern __shared__ double sm_r[];
+  int R = blockDim.x / mp;
+  int c = threadIdx.x % mp, rr = threadIdx.x / mp;
+  double sr = 0.0, sx = 0.0;
+  if (rr < R) {
+    T th = c < m ? (T)theta[c] : T(0);
+    for (int64_t row = (int64_t)blockIdx.x * R + rr; row < n; row += (int64_t)gridDim.x * R) {
+      T x = S[row * ld + c];
+      T w = T(0);
+      if (c < m) {
+        T ax = AS[row * ld + c];
+        T bx = b[row] * x;
+        T r = ax - bx * th;
+        sr += (double)r * (double)r;
+        sx += (double)x * (double)x;
+        w = prec ? prec[row] * r : r;
+      }
+      if (Wd) Wd[row * ld + wcol + c] = w;
+    }
+    sm_r[rr * 2 * mp + c] = sr;
+    sm_r[rr * 2 * mp + mp + c] = sx;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 2 * mp; t += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < R; ++q) s += sm_r[q * 2 * mp + t];
+    part[(int64_t)blockIdx.x * 2 * mp + t] = s;
+  }
+}
+
+// theta_c = X_c . (AX)_c  (eigensolver.py:230-231, 270-271: diag of X^T AX)
+template <typename T>
+__global__ void k_coldot(int64_t n, const T *__restrict__ S, const T *__restrict__ AS, int ld,
+                         int mp, double *__restrict__ part) {
+  extern __shared__ double sm_d[];
+  int R = blockDim.x / mp;
+  int c = threadIdx.x % mp, rr = threadIdx.x / mp;
+  double s = 0.0;
+  if (rr < R) {
+    for (int64_t row = (int64_t)blockIdx.x * R + rr; row < n; row += (int64_t)gridDim.x * R)
+      s += (double)S[row * ld + c] * (double)AS[row * ld + c];
+    sm_d[rr * mp + c] = s;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < mp; t += blockDim.x) {
+    double a = 0.0;
+    for (int q = 0; q < R; ++q) a += sm_d[q * mp + t];
+    part[(int64_t)blockIdx.x * mp + t] = a;
+  }
+}
+
+// (max |x|, first index) per column, for the sign convention (eigensolver.py:83-89)
+template <typename T>
+__global__ void k_colamax(int64_t n, const T *__restrict__ S, int ld, int mp,
+                          const int64_t *__restrict__ perm, double *__restrict__ pv,
+                          int64_t *__restrict__ pi, double *__restrict__ pval) {
+  extern __shared__ double sm_a[];
+  int R = blockDim.x / mp;
+  int c = threadIdx.x % mp, rr = threadIdx.x / mp;
+  double best = -1.0, bval = 0.0;
+  int64_t bi = INT64_MAX;
+  if (rr < R) {
+    for (int64_t row = (int64_t)blockIdx.x * R + rr; row < n; row += (int64_t)gridDim.x * R) {
+      double x = (double)S[row * ld + c];
+      double a = fabs(x);
+      int64_t oi = perm ? perm[row] : row;
+      if (a > best || (a == best && oi < bi)) {
+        best = a;
+        bi = oi;
+        bval = x;
+      }
+    }
+  }
+  double *sv = sm_a;
+  double *sx = sm_a + blockDim.x;
+  int64_t *si = reinterpret_cast<int64_t *>(sm_a + 2 * blockDim.x);
+  sv[threadIdx.x] = best;
+  sx[threadIdx.x] = bval;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int t = threadIdx.x; t < mp; t += blockDim.x) {
+    double b2 = -1.0, v2 = 0.0;
+    int64_t i2 = INT64_MAX;
+    for (int q = 0; q < R; ++q) {
+      int e = q * mp + t;
+      if (sv[e] > b2 || (sv[e] == b2 && si[e] < i2)) {
+        b2 = sv[e];
+        i2 = si[e];
+        v2 = sx[e];
+      }
+    }
+    pv[(int64_t)blockIdx.x * mp + t] = b2;
+    pi[(int64_t)blockIdx.x * mp + t] = i2;
+    pval[(int64_t)blockIdx.x * mp + t] = v2;
+  }
+}
+
+__global__ void k_reduce_cols(const double *__restrict__ part, int nb, int w,
+                              double *__restrict__ out) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < w; t += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < nb; ++q) s += part[(int64_t)q * w + t];
+    out[t] = s;
+  }
+}
+
+// X0 from the normal stream: S[r][c0 + c] = z[off + r*w + c]  (row-major (n, w))
+template <typename T>
+__global__ void k_load_normals(int64_t n, int w, const double *__restrict__ z, int64_t off,
+                               const int64_t *__restrict__ perm, T *__restrict__ S, int ld, int c0) {
+  int64_t total = n * (int64_t)w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / w;
+    int c = (int)(e - r * w);
+    int64_t src = perm ? perm[r] : r;
+    S[r * ld + c0 + c] = (T)z[off + src * w + c];
+  }
+}
+
+template <typename T>
+__global__ void k_set_col(int64_t n, const double *__restrict__ v, double scalar, T *S, int ld,
+                          int c) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    S[r * ld + c] = v ? (T)v[r] : (T)scalar;
+}
+
+template <typename T>
+__global__ void k_copy_cols(int64_t n, const T *__restrict__ src, int lds, int sc0, T *dst,
+                            int ldd, int dc0, int w) {
+  int64_t total = n * (int64_t)w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / w;
+    int c = (int)(e - r * w);
+    dst[r * ldd + dc0 + c] = src[r * lds + sc0 + c];
+  }
+}
+
+// Output: eig[orig][j] = sign_j * S[r][col_j]  (double, row-major n x k)
+template <typename T>
+__global__ void k_write_vectors(int64_t n, const T *__restrict__ S, int ld, int k,
+                                const int *__restrict__ cols, const double *__restrict__ sign,
+                                const int64_t *__restrict__ perm, double *__restrict__ out) {
+  int64_t total = n * (int64_t)k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / k;
+    int j = (int)(e - r * k);
+    int64_t o = perm ? perm[r] : r;
+    out[o * k + j] = sign[j] * (double)S[r * ld + cols[j]];
+  }
+}
+
+template <typename T>
+__global__ void k_vec_T(int64_t n, const double *__restrict__ x, T *__restrict__ y, int mode) {
+  // mode 0: copy, mode 1: jacobi preconditioner 1/d (d <= 0 -> 1), eigensolver.py:204-209
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = x[i];
+    if (mode == 1) v = 1.0 / (v <= 0.0 ? 1.0 : v);
+    y[i] = (T)v;
+  }
+}
+
+// ------------------------------------------------ fused transform + Gram ---
+struct GramSpec {
+  int r0 = 0, rw = 0, c0 = 0, cw = 0;
+  int sym = 0, use_as = 0;
+  int t4r = 0, t4c = 0, ntiles = 0;
+  double *part = nullptr;  // [grid][rw*cw]
+};
+
+template <typename T>
+struct PassArgs {
+  int64_t n;
+  T *S, *AS;
+  int ld;
+  const T *b;
+  int xf, xf_acc, xf_as, i0, iw, o0, ow;
+  const T *M;  // iw x ow row-major
+  int ng;
+  GramSpec g[2];
+  int tile_lo, tile_hi;
+  int load_as;
+};
+
+__device__ __forceinline__ void decode_tile(const GramSpec &g, int t, int &ti, int &tj) {
+  if (!g.sym) {
+    ti = t / g.t4c;
+    tj = t - ti * g.t4c;
+    return;
+  }
+  int r = 0;
+  while (t >= g.t4c - r) {
+    t -= g.t4c - r;
+    ++r;
+  }
+  ti = r;
+  tj = r + t;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kPassThreads) k_tile_pass(PassArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using V = typename VecT<T>::V;
+  constexpr int VN = VecT<T>::N;
+  const int ld = a.ld;
+  T *sS = reinterpret_cast<T *>(smem_raw);
+  T *sA = sS + kTR * ld + 8;
+  T *sN = sA + kTR * ld + 8;
+  T *sb = sN + kTR * (a.ow > 0 ? a.ow : 1) + 8;
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  int own_spec[kGT], own_i[kGT], own_j[kGT];
+  int nown = 0;
+#pragma unroll
+  for (int q = 0; q < kGT; ++q) {
+    int t = a.tile_lo + tid + q * nt;
+    own_spec[q] = -1;
+    if (t < a.tile_hi) {
+      int sp = 0;
+      if (a.ng > 1 && t >= a.g[0].ntiles) {
+        t -= a.g[0].ntiles;
+        sp = 1;
+      }
+      own_spec[q] = sp;
+      decode_tile(a.g[sp], t, own_i[q], own_j[q]);
+      nown = q + 1;
+    }
+  }
+  double acc[kGT][16];
+#pragma unroll
+  for (int q = 0; q < kGT; ++q)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[q][e] = 0.0;
+
+  const int64_t ntr = (a.n + kTR - 1) / kTR;
+  for (int64_t rt = blockIdx.x; rt < ntr; rt += gridDim.x) {
+    const int64_t r0 = rt * kTR;
+    const int nr = (int)min((int64_t)kTR, a.n - r0);
+    {
+      const int nv = nr * ld / VN, tv = kTR * ld / VN;
+      const V *gs = reinterpret_cast<const V *>(a.S + r0 * ld);
+      V *ss = reinterpret_cast<V *>(sS);
+      for (int e = tid; e < tv; e += nt) {
+        V z;
+        T *pz = reinterpret_cast<T *>(&z);
+#pragma unroll
+        for (int q = 0; q < VN; ++q) pz[q] = T(0);
+        ss[e] = e < nv ? gs[e] : z;
+      }
+      if (a.load_as) {
+        const V *ga = reinterpret_cast<const V *>(a.AS + r0 * ld);
+        V *sa = reinterpret_cast<V *>(sA);
+        for (int e = tid; e < tv; e += nt) {
+          V z;
+          T *pz = reinterpret_cast<T *>(&z);
+#pragma unroll
+          for (int q = 0; q < VN; ++q) pz[q] = T(0);
+          sa[e] = e < nv ? ga[e] : z;
+        }
+      }
+      for (int e = tid; e < kTR; e += nt) sb[e] = e < nr ? a.b[r0 + e] : T(0);
+    }
+    __syncthreads();
+    if (a.xf) {
+      for (int mat = 0; mat < (a.xf_as ? 2 : 1); ++mat) {
+        T *src = mat ? sA : sS;
+        T *gdst = mat ? a.AS : a.S;
+        const int ow4 = (a.ow + 3) >> 2;
+        for (int e = tid; e < kTR * ow4; e += nt) {
+          const int r = e / ow4, c = (e - r * ow4) * 4;
+          T o[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            o[q] = (a.xf_acc && c + q < a.ow) ? src[r * ld + a.o0 + c + q] : T(0);
+          const T *xr = src + r * ld + a.i0;
+          if (c + 4 <= a.ow) {
+            for (int i = 0; i < a.iw; ++i) {
+              const T x = xr[i];
+              const T *mr = a.M + (int64_t)i * a.ow + c;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) o[q] += x * __ldg(mr + q);
+            }
+          } else {
+            for (int i = 0; i < a.iw; ++i) {
+              const T x = xr[i];
+              const T *mr = a.M + (int64_t)i * a.ow + c;
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (c + q < a.ow) o[q] += x * __ldg(mr + q);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c + q < a.ow) sN[r * a.ow + c + q] = o[q];
+        }
+        __syncthreads();
+        for (int e = tid; e < kTR * a.ow; e += nt) {
+          const int r = e / a.ow, c = e - r * a.ow;
+          const T v = sN[e];
+          src[r * ld + a.o0 + c] = v;
+          if (r < nr) gdst[(r0 + r) * ld + a.o0 + c] = v;
+        }
+        __syncthreads();
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kGT; ++q) {
+      if (q >= nown || own_spec[q] < 0) continue;
+      const GramSpec &g = a.g[own_spec[q]];
+      const int ii = g.r0 + 4 * own_i[q], jj = g.c0 + 4 * own_j[q];
+      const T *Vs = g.use_as ? sA : sS;
+      T p[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) p[e] = T(0);
+      for (int r = 0; r < kTR; ++r) {
+        const T *ur = sS + r * ld + ii;
+        const T *vr = Vs + r * ld + jj;
+        T u[4], v[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          u[t] = ur[t];
+          v[t] = vr[t];
+        }
+        if (!g.use_as) {
+          const T w = sb[r];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) v[t] = w * v[t];
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) p[x * 4 + y] += u[x] * v[y];
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc[q][e] += (double)p[e];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < kGT; ++q) {
+    if (q >= nown || own_spec[q] < 0) continue;
+    const GramSpec &g = a.g[own_spec[q]];
+    double *dst = g.part + (int64_t)blockIdx.x * g.rw * g.cw;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        int i = 4 * own_i[q] + x, j = 4 * own_j[q] + y;
+        if (i < g.rw && j < g.cw) dst[i * g.cw + j] = acc[q][x * 4 + y];
+      }
+  }
+}
+
+__global__ void k_reduce_gram(const double *__restrict__ part, int nb, int rw, int cw, int sym,
+                              double *__restrict__ out) {
+  int tot = rw * cw;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
+    int i = e / cw, j = e - i * cw;
+    int src = (sym && (i >> 2) > (j >> 2)) ? j * cw + i : e;
+    double s = 0.0;
+    for (int q = 0; q < nb; ++q) s += part[(int64_t)q * tot + src];
+    out[e] = s;
+  }
+}
+
+// ------------------------------------------------------- control kernels ---
+struct ProjArgs {
+  int nx;              // projector columns: rows [0, nx) of M are live
+  int rows;            // M rows (in width)
+  int g_c0, g_cw;      // G is rows x g_cw over physical columns [g_c0, g_c0+g_cw)
+  int o0, ow;          // M columns = physical [o0, o0+ow)
+  int nv;
+  int vcols[kMaxL];    // physical columns that are projected
+  double denom;        // divide coefficients by this (> 0), else skip (eigensolver.py:95-97)
+};
+
+template <typename T>
+__global__ void k_ctrl_proj(ProjArgs a, const double *__restrict__ G, T *__restrict__ M) {
+  __shared__ unsigned char live[1024];
+  for (int c = threadIdx.x; c < a.ow; c += blockDim.x) live[c] = 0;
+  __syncthreads();
+  for (int v = threadIdx.x; v < a.nv; v += blockDim.x) {
+    int c = a.vcols[v] - a.o0;
+    if (c >= 0 && c < a.ow) live[c] = 1;
+  }
+  __syncthreads();
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < a.rows * a.ow;
+       e += gridDim.x * blockDim.x) {
+    int x = e / a.ow, c = e - x * a.ow;
+    double v = 0.0;
+    if (x < a.nx && live[c] && a.denom > 0.0) v = -G[x * a.g_cw + (a.o0 + c - a.g_c0)] / a.denom;
+    M[e] = (T)v;
+  }
+}
+
+struct CholArgs {
+  int nl;
+  int order[kMaxL];    // logical -> physical column
+  int g0, gw;          // G over physical [g0, g0+gw)
+  double maxnorm0;
+  int in0, iw, o0, ow; // M rows physical [in0, in0+iw), cols -> new basis slots [0, ow)
+  int use_global;      // matrices in global scratch instead of shared memory
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kCtrlThreads)
+    k_ctrl_chol(CholArgs a, const double *__restrict__ G, T *__restrict__ M, int *status,
+                double *scratch) {
+  extern __shared__ __align__(16) double smc[];
+  __shared__ int keep[kMaxL];
+  __shared__ int rank[kMaxL];
+  __shared__ double dummy;
+  const int nl = a.nl, tid = threadIdx.x, nt = blockDim.x;
+  double *Gl = a.use_global ? scratch : smc;
+  double *R = Gl + nl * nl;
+  double *Ri = a.use_global ? R + nl * nl : Gl;  // Rinv overwrites Gl after the factorisation
+  for (int e = tid; e < nl * nl; e += nt) {
+    int x = e / nl, y = e - x * nl;
+    Gl[e] = G[(a.order[x] - a.g0) * a.gw + (a.order[y] - a.g0)];
+  }
+  __syncthreads();
+  int nk = blk_cholesky_drop(Gl, nl, nl, a.maxnorm0, R, nl, keep, &dummy);
+  blk_tri_inv_kept(R, nl, nl, keep, Ri, nl);
+  if (tid == 0) {
+    int r = 0;
+    for (int t = 0; t < nl; ++t) rank[t] = keep[t] ? r++ : -1;
+    status[0] = nk;
+  }
+  for (int e = tid; e < a.iw * a.ow; e += nt) M[e] = T(0);
+  __syncthreads();
+  for (int e = tid; e < nl * nl; e += nt) {
+    int x = e / nl, t = e - x * nl;
+    if (!keep[t] || !keep[x] || x > t) continue;
+    int row = a.order[x] - a.in0;
+    int col = rank[t];
+    if (row >= 0 && row < a.iw && col < a.ow) M[row * a.ow + col] = (T)Ri[x * nl + t];
+  }
+}
+
+struct RRArgs {
+  int px;        // trusted prefix columns at physical [0, px) (X, already B-orthonormal)
+  int v0, vw;    // new basis V1 at physical [v0, v0+nk), its B-Gram G4 is vw x vw
+  int hw;        // A-Gram H covers physical [0, hw)
+  int m, mp;     // block size, padded
+  int want_p;
+  int use_global;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kCtrlThreads)
+    k_ctrl_rr(RRArgs a, const double *__restrict__ G4, const double *__restrict__ H,
+              T *__restrict__ M5, double *__restrict__ theta, int *status, double *scratch) {
+  extern __shared__ __align__(16) double smr[];
+  __shared__ int keep[kMaxL];
+  __shared__ int rank[kMaxL];
+  __shared__ int perm[kMaxL];
+  __shared__ int pidx[kMaxL + 2];
+  __shared__ double cs[kMaxL + 2];
+  __shared__ double w[kMaxL];
+  __shared__ double red[kCtrlThreads];
+  __shared__ int cnt;
+  __shared__ double dummy;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int nk = status[0];
+  // scratch layout (global): F [hw x smax], HF [hw x smax], (+ big matrices if use_global)
+  const int smax = a.px + nk;
+  double *F = scratch;
+  double *HF = F + (int64_t)a.hw * smax;
+  double *big = HF + (int64_t)a.hw * smax;
+  double *W1 = a.use_global ? big : smr;
+  double *R2 = W1 + nk * nk;
+  // 1. second CholQR pass on V1 (B-Gram G4)
+  for (int e = tid; e < nk * nk; e += nt) {
+    int x = e / nk, y = e - x * nk;
+    W1[e] = G4[x * a.vw + y];
+  }
+  __syncthreads();
+  int nk2 = blk_cholesky_drop(W1, nk, nk, 0.0, R2, nk, keep, &dummy);
+  blk_tri_inv_kept(R2, nk, nk, keep, W1, nk);  // W1 <- R2^-1
+  if (tid == 0) {
+    int r = 0;
+    for (int t = 0; t < nk; ++t) rank[t] = keep[t] ? r++ : -1;
+  }
+  __syncthreads();
+  const int s = a.px + nk2;
+  // 2. F: S_final = B0 F  (B0 = physical [0, hw))
+  for (int e = tid; e < a.hw * s; e += nt) F[e] = 0.0;
+  __syncthreads();
+  for (int c = tid; c < a.px; c += nt) F[c * s + c] = 1.0;
+  for (int e = tid; e < nk * nk; e += nt) {
+    int u = e / nk, t = e - u * nk;
+    if (keep[t] && keep[u] && u <= t) F[(a.v0 + u) * s + a.px + rank[t]] = W1[u * nk + t];
+  }
+  __syncthreads();
+  // 3. HF = H F ; G_RR = F^T HF (symmetrised, eigensolver.py:252)
+  for (int e = tid; e < a.hw * s; e += nt) {
+    int i = e / s, j = e - i * s;
+    double acc = 0.0;
+    for (int u = 0; u < a.hw; ++u) {
+      double f = F[u * s + j];
+      if (f != 0.0) acc += H[i * a.hw + u] * f;
+    }
+    HF[e] = acc;
+  }
+  __syncthreads();
+  double *Aj = a.use_global ? big + 2 * nk * nk : smr;
+  double *Vj = Aj + s * s;
+  for (int e = tid; e < s * s; e += nt) {
+    int i = e / s, j = e - i * s;
+    double acc = 0.0;
+    for (int u = 0; u < a.hw; ++u) {
+      double f = F[u * s + i];
+      if (f != 0.0) acc += f * HF[u * s + j];
+    }
+    Aj[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < s * s; e += nt) {
+    int i = e / s, j = e - i * s;
+    if (i < j) {
+      double v = 0.5 * (Aj[i * s + j] + Aj[j * s + i]);
+      Aj[i * s + j] = v;
+      Aj[j * s + i] = v;
+    }
+  }
+  __syncthreads();
+  blk_jacobi(Aj, s, s, Vj, s, w, cs, pidx, perm, &cnt, red);
+  const int take = min(a.m, s);
+  for (int i = tid; i < take; i += nt) theta[i] = w[i];
+  // 4. M5 = [F Y | F[:, m:] Y[m:]]   (rows physical [0, hw), cols [0, 2mp))
+  const int ow = 2 * a.mp;
+  for (int e = tid; e < a.hw * ow; e += nt) {
+    int r = e / ow, c = e - r * ow;
+    double acc = 0.0;
+    if (c < take) {
+      int col = perm[c];
+      for (int u = 0; u < s; ++u) acc += F[r * s + u] * Vj[u * s + col];
+    } else if (a.want_p && c >= a.mp && c - a.mp < take) {
+      int col = perm[c - a.mp];
+      for (int u = a.m; u < s; ++u) acc += F[r * s + u] * Vj[u * s + col];
+    }
+    M5[e] = (T)acc;
+  }
+  if (tid == 0) {
+    status[1] = take;
+    status[2] = nk2;
+    status[3] = s;
+  }
+}
+
+// ------------------------------------------------------------ the solver ---
+template <typename T>
+struct Lobpcg {
+  static constexpr int VN = VecT<T>::N;
+  mg_ctx *ctx;
+  const DevCSR<T> &A;
+  const SolveSpec &sp;
+  int64_t n;
+  int m, mp, ld;
+  int grid_pass;
+  DBuf<T> S, AS, bw, prec, M, tmpblk;
+  DBuf<double> part0, part1, Gr0, Gr1, theta, colpart, colred, scratch;
+  DBuf<int> status;
+  double anorm = 0, bmax = 0, ydenom = 0;
+  int64_t zpos = 0;
+  bool have_y = false;
+
+  Lobpcg(mg_ctx *c, const DevCSR<T> &a, const SolveSpec &s) : ctx(c), A(a), sp(s), n(a.n) {
+    m = s.k;
+    mp = (m + VN - 1) / VN * VN;
+    ld = 3 * mp + VN;
+  }
+
+  size_t pass_smem(int ow) const {
+    return (size_t)(3 * kTR * ld + kTR * (ow > 0 ? ow : 1) + 4 * 8 + kTR) * sizeof(T) + 64;
+  }
+
+  // run one tile pass: optional transform, then up to two Gram products
+  void pass(int xf, int xf_acc, int xf_as, int i0, int iw, int o0, int ow, GramSpec *g, int ng,
+            double *red0, double *red1) {
+    PassArgs<T> a{};
+    a.n = n;
+    a.S = S.p;
+    a.AS = AS.p;
+    a.ld = ld;
+    a.b = bw.p;
+    a.xf = xf;
+    a.xf_acc = xf_acc;
+    a.xf_as = xf_as;
+    a.i0 = i0;
+    a.iw = iw;
+    a.o0 = o0;
+    a.ow = xf ? ow : 0;
+    a.M = M.p;
+    a.ng = ng;
+    int total = 0;
+    a.load_as = xf_as;
+    for (int q = 0; q < ng; ++q) {
+      GramSpec &s = g[q];
+      s.t4r = (s.rw + 3) / 4;
+      s.t4c = (s.cw + 3) / 4;
+      s.ntiles = s.sym ? s.t4r * (s.t4r + 1) / 2 : s.t4r * s.t4c;
+      s.part = q == 0 ? part0.p : part1.p;
+      a.g[q] = s;
+      total += s.ntiles;
+      if (s.use_as) a.load_as = 1;
+    }
+    size_t smem = pass_smem(a.ow);
+    const int cap = kPassThreads * kGT;
+    int lo = 0;
+    bool first = true;
+    do {
+      a.tile_lo = lo;
+      a.tile_hi = std::min(total, lo + cap);
+      if (!first) {
+        a.xf = 0;
+        a.ow = 0;
+      }
+      k_tile_pass<T><<<grid_pass, kPassThreads, smem, ctx->stream>>>(a);
+      MG_CHECK_LAUNCH(ctx);
+      first = false;
+      lo += cap;
+    } while (lo < total);
+    double *reds[2] = {red0, red1};
+    for (int q = 0; q < ng; ++q) {
+      int tot = g[q].rw * g[q].cw;
+      k_reduce_gram<<<grid_for(tot, 256, 4 * ctx->num_sms), 256, 0, ctx->stream>>>(
+          a.g[q].part, grid_pass, g[q].rw, g[q].cw, g[q].sym, reds[q]);
+      MG_CHECK_LAUNCH(ctx);
+    }
+  }
+
+  GramSpec gspec(int r0, int rw, int c0, int cw, int sym, int use_as) {
+    GramSpec s;
+    s.r0 = r0; s.rw = rw; s.c0 = c0; s.cw = cw; s.sym = sym; s.use_as = use_as;
+    return s;
+  }
+
+  void spmm_cols(int c0, int w) { spmm<T>(ctx, A, S.p + c0, ld, AS.p + c0, ld, w); }
+
+  // per-column reductions: returns host [rn^2 (mp) | qn^2 (mp)]
+  void resid(bool write_w, std::vector<double> &out) {
+    int R = std::max(1, 256 / mp);
+    int bs = R * mp;
+    int nb = grid_for(n, R, ctx->num_sms * 4);
+    size_t sm = (size_t)R * 2 * mp * sizeof(double);
+    k_resid<T><<<nb, bs, sm, ctx->stream>>>(n, S.p, AS.p, ld, m, mp, 2 * mp, theta.p, bw.p,
+                                            sp.jacobi ? prec.p : nullptr, write_w ? S.p : nullptr,
+                                            colpart.p);
+    MG_CHECK_LAUNCH(ctx);
+    k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, nb, 2 * mp, colred.p);
+    MG_CHECK_LAUNCH(ctx);
+    out.resize(2 * mp);
+    d2h_sync(ctx, out.data(), colred.p, 2 * mp * sizeof(double));
+  }
+
+  // theta_c = X_c . AX_c, stored on the device theta array; also returned
+  void fresh_theta(std::vector<double> &th) {
+    spmm_cols(0, mp);
+    int R = std::max(1, 256 / mp);
+    int nb = grid_for(n, R, ctx->num_sms * 4);
+    k_coldot<T><<<nb, R * mp, (size_t)R * mp * sizeof(double), ctx->stream>>>(n, S.p, AS.p, ld,
+                                                                              mp, colpart.p);
+    MG_CHECK_LAUNCH(ctx);
+    k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, nb, mp, theta.p);
+    MG_CHECK_LAUNCH(ctx);
+    th.resize(mp);
+    d2h_sync(ctx, th.data(), theta.p, mp * sizeof(double));
+  }
+
+  // project y out of physical columns [c_lo, c_hi) (eigensolver.py:92-99)
+  void deflate_cols(int c_lo, int c_hi, int region0, int region_w) {
+    if (!have_y) return;
+    GramSpec g = gspec(3 * mp, 1, region0, region_w, 0, 0);
+    pass(0, 0, 0, 0, 0, 0, 0, &g, 1, Gr0.p, nullptr);
+    ProjArgs pa{};
+    pa.nx = 1;
+    pa.rows = 1;
+    pa.g_c0 = region0;
+    pa.g_cw = region_w;
+    pa.o0 = region0;
+    pa.ow = region_w;
+    pa.nv = 0;
+    for (int c = c_lo; c < c_hi; ++c) pa.vcols[pa.nv++] = c;
+    pa.denom = ydenom;
+    k_ctrl_proj<T><<<1, 256, 0, ctx->stream>>>(pa, Gr0.p, M.p);
+    MG_CHECK_LAUNCH(ctx);
+    pass(1, 1, 0, 3 * mp, 1, region0, region_w, nullptr, 0, nullptr, nullptr);
+  }
+
+  size_t chol_smem(int nl, int &use_global) const {
+    size_t need = (size_t)2 * nl * nl * sizeof(double);
+    use_global = need > 200 * 1024;
+    return use_global ? 0 : need;
+  }
+
+  // B-orthonormalise `order` (physical columns) over G covering [g0, g0+gw);
+  // writes the new basis into [o0, o0+ow).  Returns nothing (nk on device).
+  void ortho(const std::vector<int> &order, int g0, int gw, double maxnorm0, int in0, int iw,
+             int o0, int ow) {
+    CholArgs ca{};
+    ca.nl = (int)order.size();
+    require(ca.nl <= kMaxL, MG_ERR_INPUT, "block too wide");
+    for (int i = 0; i < ca.nl; ++i) ca.order[i] = order[i];
+    ca.g0 = g0;
+    ca.gw = gw;
+    ca.maxnorm0 = maxnorm0;
+    ca.in0 = in0;
+    ca.iw = iw;
+    ca.o0 = o0;
+    ca.ow = ow;
+    int ug = 0;
+    size_t sm = chol_smem(ca.nl, ug);
+    ca.use_global = ug;
+    if (sm > 48 * 1024)
+      MG_CUDA(cudaFuncSetAttribute(k_ctrl_chol<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sm));
+    k_ctrl_chol<T><<<1, kCtrlThreads, sm, ctx->stream>>>(ca, Gr0.p, M.p, status.p, scratch.p);
+    MG_CHECK_LAUNCH(ctx);
+  }
+
+  void rr(int px, int v0, int vw, int hw, bool want_p) {
+    RRArgs ra{};
+    ra.px = px;
+    ra.v0 = v0;
+    ra.vw = vw;
+    ra.hw = hw;
+    ra.m = m;
+    ra.mp = mp;
+    ra.want_p = want_p;
+    int smax = px + vw;
+    size_t need = (size_t)2 * std::max(smax * smax, vw * vw) * sizeof(double);
+    ra.use_global = need > 200 * 1024;
+    size_t sm = ra.use_global ? 0 : need;
+    if (sm > 48 * 1024)
+      MG_CUDA(cudaFuncSetAttribute(k_ctrl_rr<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sm));
+    k_ctrl_rr<T><<<1, kCtrlThreads, sm, ctx->stream>>>(ra, Gr0.p, Gr1.p, M.p, theta.p, status.p,
+                                                       scratch.p);
+    MG_CHECK_LAUNCH(ctx);
+  }
+
+  int read_status(int i) {
+    int v[4];
+    d2h_sync(ctx, v, status.p, sizeof(v));
+    return v[i];
+  }
+
+  void place_normals(int c0, int w) {
+    int64_t need = n * (int64_t)w;
+    require(sp.normals != nullptr && zpos + need <= sp.n_normals, MG_ERR_INPUT,
+            "standard-normal stream exhausted (need " + std::to_string(zpos + need) + ", have " +
+                std::to_string(sp.n_normals) + ")");
+    k_load_normals<T><<<grid_for(need, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        n, w, sp.normals, zpos, sp.perm, S.p, ld, c0);
+    MG_CHECK_LAUNCH(ctx);
+    zpos += need;
+  }
+
+  // orth_pair([X], [AX]) with refills, then the plain Rayleigh-Ritz of
+  // eigensolver.py:196-200 / 261-265.  X has `have` valid columns at [0, have).
+  void orth_refill_rr(int have) {
+    int cur = have;
+    while (true) {
+      std::vector<int> order(cur);
+      std::iota(order.begin(), order.end(), 0);
+      GramSpec g = gspec(0, mp, 0, mp, 1, 0);
+      pass(0, 0, 0, 0, 0, 0, 0, &g, 1, Gr0.p, nullptr);
+      ortho(order, 0, mp, 0.0, 0, mp, 0, mp);
+      pass(1, 0, 1, 0, mp, 0, mp, nullptr, 0, nullptr, nullptr);  // V1 -> [0, nk)
+      int nk = read_status(0);
+      if (nk >= m) break;
+      // refill (eigensolver.py:188-193): extra = stream (n, m-nk), deflated, + A-images
+      place_normals(nk, m - nk);
+      deflate_cols(nk, m, 0, mp);
+      spmm<T>(ctx, A, S.p, ld, tmpblk.p, mp, mp);
+      k_copy_cols<T><<<grid_for(n * (m - nk), 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          n, tmpblk.p, mp, nk, AS.p, ld, nk, m - nk);
+      MG_CHECK_LAUNCH(ctx);
+      cur = m;
+    }
+    GramSpec g[2] = {gspec(0, mp, 0, mp, 1, 0), gspec(0, mp, 0, mp, 1, 1)};
+    pass(0, 0, 0, 0, 0, 0, 0, g, 2, Gr0.p, Gr1.p);
+    rr(0, 0, mp, mp, false);
+    // M5 is hw x 2mp: X <- [0,mp), zero P region (P = None)
+    pass(1, 0, 1, 0, mp, 0, 2 * mp, nullptr, 0, nullptr, nullptr);
+  }
+
+  // residual pass + one D2H of [rn^2 | qn^2 | theta | status]
+  void iterate_sync(bool write_w, std::vector<double> &cr, std::vector<double> &th, int st[4]) {
+    int R = std::max(1, 256 / mp);
+    int bs = R * mp;
+    int nb = grid_for(n, R, ctx->num_sms * 4);
+    size_t sm = (size_t)R * 2 * mp * sizeof(double);
+    k_resid<T><<<nb, bs, sm, ctx->stream>>>(n, S.p, AS.p, ld, m, mp, 2 * mp, theta.p, bw.p,
+                                            sp.jacobi ? prec.p : nullptr, write_w ? S.p : nullptr,
+                                            colpart.p);
+    MG_CHECK_LAUNCH(ctx);
+    k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, nb, 2 * mp, colred.p);
+    MG_CHECK_LAUNCH(ctx);
+    MG_CUDA(cudaMemcpyAsync(colred.p + 2 * mp, theta.p, mp * sizeof(double),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+    MG_CUDA(cudaMemcpyAsync(colred.p + 3 * mp, status.p, 4 * sizeof(int), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    std::vector<double> buf(3 * mp + 2);
+    d2h_sync(ctx, buf.data(), colred.p, buf.size() * sizeof(double));
+    cr.assign(buf.begin(), buf.begin() + 2 * mp);
+    th.assign(buf.begin() + 2 * mp, buf.begin() + 3 * mp);
+    std::memcpy(st, buf.data() + 3 * mp, 4 * sizeof(int));
+  }
+
+  SolveResult run(double anorm_in, const double *b_dev, const double *diag_dev, double *eigvecs) {
+    SolveResult res;
+    require(m >= 1, MG_ERR_INPUT, "block size must be >= 1, got " + std::to_string(m));
+    require(m <= n, MG_ERR_INPUT,
+            "block size " + std::to_string(m) + " exceeds dimension " + std::to_string(n));
+    require(3 * mp + VN <= kMaxL, MG_ERR_INPUT, "block size too large for this build");
+    anorm = anorm_in;
+    int64_t ntiles = (n + kTR - 1) / kTR;
+    grid_pass = (int)std::min<int64_t>(ntiles, 2 * ctx->num_sms);
+    S.alloc(ctx, n * ld);
+    AS.alloc(ctx, n * ld);
+    S.zero();
+    AS.zero();
+    bw.alloc(ctx, n);
+    prec.alloc(ctx, n);
+    tmpblk.alloc(ctx, n * mp);
+    int g = grid_for(n, 256, ctx->num_sms * 16);
+    k_vec_T<T><<<g, 256, 0, ctx->stream>>>(n, b_dev, bw.p, 0);
+    MG_CHECK_LAUNCH(ctx);
+    k_vec_T<T><<<g, 256, 0, ctx->stream>>>(n, diag_dev, prec.p, 1);
+    MG_CHECK_LAUNCH(ctx);
+    int wmax = 3 * mp + VN;
+    M.alloc(ctx, (size_t)wmax * wmax);
+    part0.alloc(ctx, (size_t)grid_pass * wmax * wmax);
+    part1.alloc(ctx, (size_t)grid_pass * wmax * wmax);
+    Gr0.alloc(ctx, (size_t)wmax * wmax);
+    Gr1.alloc(ctx, (size_t)wmax * wmax);
+    theta.alloc(ctx, wmax);
+    theta.zero();
+    colpart.alloc(ctx, (size_t)ctx->num_sms * 4 * 2 * wmax);
+    colred.alloc(ctx, 4 * wmax + 8);
+    scratch.alloc(ctx, (size_t)8 * wmax * wmax + 4096);
+    status.alloc(ctx, 8);
+    status.zero();
+    size_t smax_pass = pass_smem(3 * mp);
+    MG_CUDA(cudaFuncSetAttribute(k_tile_pass<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smax_pass));
+    bmax = max_f64_const(ctx, b_dev, n);
+    have_y = sp.deflate != nullptr;
+    if (have_y) {  // deflation vector y at column 3mp, and y'By
+      k_set_col<T><<<g, 256, 0, ctx->stream>>>(n, sp.deflate, 0.0, S.p, ld, 3 * mp);
+      MG_CHECK_LAUNCH(ctx);
+      GramSpec gy = gspec(3 * mp, 1, 3 * mp, 1, 0, 0);
+      pass(0, 0, 0, 0, 0, 0, 0, &gy, 1, Gr0.p, nullptr);
+      d2h_sync(ctx, &ydenom, Gr0.p, sizeof(double));
+    }
+
+    // ---- initial block (eigensolver.py:177-200)
+    zpos = 0;
+    place_normals(0, m);
+    deflate_cols(0, m, 0, mp);
+    spmm_cols(0, mp);
+    orth_refill_rr(m);
+    int pcount = 0;
+    std::vector<double> cr, th;
+    const double tol = sp.tol;
+    auto conv_test = [&](std::vector<double> &rn, std::vector<int> &cv) {
+      rn.assign(m, 0.0);
+      cv.assign(m, 0);
+      for (int c = 0; c < m; ++c) {
+        rn[c] = std::sqrt(cr[c]);
+        double qn = std::sqrt(cr[mp + c]);
+        cv[c] = rn[c] <= tol * ((anorm + std::fabs(th[c]) * bmax) * qn) ? 1 : 0;
+      }
+      return std::all_of(cv.begin(), cv.end(), [](int v) { return v != 0; });
+    };
+    std::vector<double> rn;
+    std::vector<int> cv;
+    int st[4] = {m, m, m, m};
+    int it = 0;
+    for (it = 1; it <= sp.max_iter; ++it) {
+      iterate_sync(true, cr, th, st);
+      if (it > 1 && st[1] < m) {  // basis collapsed last iteration (eigensolver.py:260-266)
+        orth_refill_rr(st[1]);
+        pcount = 0;
+        iterate_sync(true, cr, th, st);
+      }
+      bool all = conv_test(rn, cv);
+      double ts = 0.0;
+      for (int c = 0; c < m; ++c) ts += th[c];
+      res.history.push_back(ts);
+      if (all) {  // re-verify against a fresh product (eigensolver.py:227-234)
+        std::vector<double> th2;
+        fresh_theta(th2);
+        iterate_sync(true, cr, th, st);
+        if (conv_test(rn, cv)) break;
+      }
+      std::vector<int> vcols;
+      for (int c = 0; c < m; ++c)
+        if (!cv[c]) vcols.push_back(2 * mp + c);
+      deflate_cols(2 * mp, 3 * mp, 2 * mp, mp);
+      spmm_cols(2 * mp, mp);
+      for (int c = 0; c < pcount; ++c) vcols.push_back(mp + c);
+      const bool prefix = (it % 32) != 0;
+      if (prefix) {
+        for (int rep = 0; rep < 2; ++rep) {
+          if (rep == 0) {
+            GramSpec gp = gspec(0, mp, mp, 2 * mp, 0, 0);
+            pass(0, 0, 0, 0, 0, 0, 0, &gp, 1, Gr0.p, nullptr);
+          }
+          ProjArgs pa{};
+          pa.nx = m;
+          pa.rows = mp;
+          pa.g_c0 = mp;
+          pa.g_cw = 2 * mp;
+          pa.o0 = mp;
+          pa.ow = 2 * mp;
+          pa.nv = (int)vcols.size();
+          for (int i = 0; i < pa.nv; ++i) pa.vcols[i] = vcols[i];
+          pa.denom = 1.0;
+          k_ctrl_proj<T><<<1, 256, 0, ctx->stream>>>(pa, Gr0.p, M.p);
+          MG_CHECK_LAUNCH(ctx);
+          GramSpec gn = rep == 0 ? gspec(0, mp, mp, 2 * mp, 0, 0)
+                                 : gspec(mp, 2 * mp, mp, 2 * mp, 1, 0);
+          pass(1, 1, 1, 0, mp, mp, 2 * mp, &gn, 1, Gr0.p, nullptr);
+        }
+        ortho(vcols, mp, 2 * mp, 1.0, mp, 2 * mp, mp, 2 * mp);
+        GramSpec g2[2] = {gspec(mp, 2 * mp, mp, 2 * mp, 1, 0),
+                          gspec(0, 3 * mp, 0, 3 * mp, 1, 1)};
+        pass(1, 0, 1, mp, 2 * mp, mp, 2 * mp, g2, 2, Gr0.p, Gr1.p);
+        rr(m, mp, 2 * mp, 3 * mp, true);
+      } else {
+        std::vector<int> order;
+        for (int c = 0; c < m; ++c) order.push_back(c);
+        for (int v : vcols) order.push_back(v);
+        GramSpec gf = gspec(0, 3 * mp, 0, 3 * mp, 1, 0);
+        pass(0, 0, 0, 0, 0, 0, 0, &gf, 1, Gr0.p, nullptr);
+        ortho(order, 0, 3 * mp, 0.0, 0, 3 * mp, 0, 3 * mp);
+        GramSpec g2[2] = {gspec(0, 3 * mp, 0, 3 * mp, 1, 0), gspec(0, 3 * mp, 0, 3 * mp, 1, 1)};
+        pass(1, 0, 1, 0, 3 * mp, 0, 3 * mp, g2, 2, Gr0.p, Gr1.p);
+        rr(0, 0, 3 * mp, 3 * mp, true);
+      }
+      pass(1, 0, 1, 0, 3 * mp, 0, 2 * mp, nullptr, 0, nullptr, nullptr);
+      pcount = m;  // corrected at the next sync if the basis collapsed
+    }
+    if (it > sp.max_iter) {
+      it = sp.max_iter;
+      if (it >= 1) {
+        int s2[4];
+        d2h_sync(ctx, s2, status.p, sizeof(s2));
+        if (s2[1] < m) orth_refill_rr(s2[1]);
+      }
+    }
+    res.iterations = it;
+    // ---- honest final report (eigensolver.py:268-283)
+    fresh_theta(th);
+    iterate_sync(false, cr, th, st);
+    conv_test(rn, cv);
+    std::vector<int> order(m);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return th[x] < th[y]; });
+    res.eigenvalues.resize(m);
+    res.residual_norms.resize(m);
+    res.converged.resize(m);
+    for (int j = 0; j < m; ++j) {
+      res.eigenvalues[j] = th[order[j]];
+      res.residual_norms[j] = rn[order[j]];
+      res.converged[j] = cv[order[j]];
+    }
+    // sign convention (eigensolver.py:83-89): largest |entry| positive, first index on ties
+    int R = std::max(1, 256 / mp);
+    int nb = grid_for(n, R, ctx->num_sms * 4);
+    DBuf<double> pv(ctx, (size_t)nb * mp), pval(ctx, (size_t)nb * mp);
+    DBuf<int64_t> pi(ctx, (size_t)nb * mp);
+    k_colamax<T><<<nb, R * mp, (size_t)R * mp * 3 * sizeof(double), ctx->stream>>>(
+        n, S.p, ld, mp, sp.perm, pv.p, pi.p, pval.p);
+    MG_CHECK_LAUNCH(ctx);
+    std::vector<double> hv((size_t)nb * mp), hval((size_t)nb * mp);
+    std::vector<int64_t> hi((size_t)nb * mp);
+    d2h_sync(ctx, hv.data(), pv.p, hv.size() * sizeof(double));
+    d2h_sync(ctx, hval.data(), pval.p, hval.size() * sizeof(double));
+    d2h_sync(ctx, hi.data(), pi.p, hi.size() * sizeof(int64_t));
+    std::vector<double> sign(m);
+    std::vector<int> cols(m);
+    for (int j = 0; j < m; ++j) {
+      int c = order[j];
+      double best = -1.0, val = 0.0;
+      int64_t bi = INT64_MAX;
+      for (int q = 0; q < nb; ++q) {
+        double v = hv[(size_t)q * mp + c];
+        int64_t ii = hi[(size_t)q * mp + c];
+        if (v > best || (v == best && ii < bi)) {
+          best = v;
+          bi = ii;
+          val = hval[(size_t)q * mp + c];
+        }
+      }
+      sign[j] = val < 0.0 ? -1.0 : 1.0;
+      cols[j] = c;
+    }
+    DBuf<double> dsign(ctx, m);
+    DBuf<int> dcols(ctx, m);
+    MG_CUDA(cudaMemcpyAsync(dsign.p, sign.data(), m * sizeof(double), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    MG_CUDA(cudaMemcpyAsync(dcols.p, cols.data(), m * sizeof(int), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    k_write_vectors<T><<<grid_for(n * m, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        n, S.p, ld, m, dcols.p, dsign.p, sp.perm, eigvecs);
+    MG_CHECK_LAUNCH(ctx);
+    sync(ctx);
+    res.normals_used = zpos;
+    return res;
+  }
+};
+
+template <typename T>
+SolveResult lobpcg(mg_ctx *ctx, const DevCSR<T> &A, double anorm, const double *b_dev,
+                   const double *diagA_dev, const SolveSpec &spec, double *eigvecs) {
+  Lobpcg<T> s(ctx, A, spec);
+  return s.run(anorm, b_dev, diagA_dev, eigvecs);
+}
+
+template void make_solver_csr<float>(mg_ctx *, int64_t, const int64_t *, const int64_t *,
+                                     const double *, OwnedCSR<float> &, int64_t);
+template void make_solver_csr<double>(mg_ctx *, int64_t, const int64_t *, const int64_t *,
+                                      const double *, OwnedCSR<double> &, int64_t);
+template void spmm<float>(mg_ctx *, const DevCSR<float> &, const float *, int, float *, int, int);
+template void spmm<double>(mg_ctx *, const DevCSR<double> &, const double *, int, double *, int,
+                           int);
+template SolveResult lobpcg<float>(mg_ctx *, const DevCSR<float> &, double, const double *,
+                                   const double *, const SolveSpec &, double *);
+template SolveResult lobpcg<double>(mg_ctx *, const DevCSR<double> &, double, const double *,
+                                    const double *, const SolveSpec &, double *);
+
+}  // namespace mg

@@ -1,0 +1,189 @@
+"""GPU parity: the sm_100a path vs the CPU oracle and the reference's golden vectors.
+
+Bars (BASELINE.json north_star): Q/A/T structure bit-exact; Q/L/A values
+bit-exact in fp64 (eps/mu pinned); b within 1e-15 relative; eigenvalues
+within 1e-8 relative (fp64) and principal angles below 1e-6 rad.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import graph_from_golden, principal_angles
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["path5", "path10", "star4", "complete5", "ring6", "ring9", "grid4x5", "twocomp",
+         "rand700"] + [f"rand{i}" for i in range(12)]
+
+
+@pytest.fixture(scope="module")
+def mg():
+    import paper_2112_07862_b200 as mg
+    return mg
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_operator_pieces_bit_exact(mg, golden_small, name):
+    z, meta = golden_small
+    n, ptr, idx, w = graph_from_golden(z, name)
+    g = mg.Graph(n, ptr, idx, w)
+    l = mg.laplacian(g)
+    assert np.array_equal(l.indptr, z[f"{name}/pair/L_ptr"])
+    assert np.array_equal(l.indices, z[f"{name}/pair/L_idx"])
+    assert np.array_equal(l.data, z[f"{name}/pair/L_val"])
+    t = mg.two_hop_sets(g)
+    assert np.array_equal(t.indptr, z[f"{name}/pair/T_ptr"])
+    assert np.array_equal(t.indices, z[f"{name}/pair/T_idx"])
+    for lit, key in ((False, "Q"), (True, "QL")):
+        q = mg.two_hop_laplacian(t, literal_diagonal=lit)
+        assert np.array_equal(q.indptr, z[f"{name}/pair/{key}_ptr"])
+        assert np.array_equal(q.indices, z[f"{name}/pair/{key}_idx"])
+        assert np.array_equal(q.data, z[f"{name}/pair/{key}_val"])
+    q = mg.two_hop_laplacian(t)
+    rec = meta[f"{name}/pair"]
+    eps = mg.identity_shift(q)
+    assert abs(eps - rec["eps"]) <= 1e-10 * max(abs(rec["eps"]), 1e-300)
+    mu = mg.repulsion_weight(l, q, rec["eps"])
+    assert mu == rec["mu"]
+    a = mg.assemble_operator(l, q, rec["mu"], rec["eps"])
+    assert np.array_equal(a.indptr, z[f"{name}/pair/A_ptr"])
+    assert np.array_equal(a.indices, z[f"{name}/pair/A_idx"])
+    assert np.array_equal(a.data, z[f"{name}/pair/A_val"])
+    if "b_error" in rec:
+        with pytest.raises(mg.DisconnectedGraphError):
+            mg.degree_balancing(a)
+    else:
+        bs = mg.degree_balancing(a)
+        ref_b = z[f"{name}/pair/b"]
+        assert np.max(np.abs(bs.b - ref_b) / ref_b) <= 4e-15
+        assert bs.generalized_degree == pytest.approx(rec["generalized_degree"], rel=1e-14)
+        pair = mg.OperatorPair(A=a, B=bs, mu=mu, epsilon=rec["eps"], Q=q)
+        d = pair.diagnostics()
+        assert d["binding_row"] == rec["diagnostics"]["binding_row"]
+        assert d["min_disc_left_end"] == rec["diagnostics"]["min_disc_left_end"]
+        assert d["q_nnz"] == rec["diagnostics"]["q_nnz"]
+
+
+def test_isolated_node_raises(mg, golden_small):
+    z, meta = golden_small
+    g = mg.Graph(*graph_from_golden(z, "isolated3"))
+    a = mg.assemble_operator(mg.laplacian(g), mg.two_hop_laplacian(mg.two_hop_sets(g)), 0.0, 0.0)
+    with pytest.raises(mg.DisconnectedGraphError, match="connected component"):
+        mg.degree_balancing(a)
+
+
+def test_reference_error_contract(mg):
+    z = mg.SparseSymMatrix.zeros(3)
+    assert np.array_equal(mg.assemble_operator(z, z, 0.0, 2.0).to_dense(), 2.0 * np.eye(3))
+    with pytest.raises(mg.InputError):
+        mg.assemble_operator(mg.SparseSymMatrix.zeros(3), mg.SparseSymMatrix.zeros(4), 0, 0)
+    q = mg.SparseSymMatrix.from_coo(2, [0], [1], [1.0])
+    with pytest.raises(mg.InputError, match="symmetric"):
+        mg.identity_shift(q)
+    omega = 0.7
+    q2 = mg.SparseSymMatrix.from_coo(2, [0, 0, 1, 1], [0, 1, 0, 1], [omega, -omega, -omega, omega])
+    assert mg.identity_shift(q2) == pytest.approx(2 * omega, rel=1e-12)
+    with pytest.raises(mg.InputError):
+        mg.repulsion_weight(q2, q2, -1.0)
+    with pytest.raises(mg.InputError):
+        mg.SolverConfig(k=0)
+    a = mg.SparseSymMatrix.from_coo(3, [0, 1, 2], [0, 1, 2], [1.0, 2.0, 3.0])
+    with pytest.raises(mg.InputError):
+        mg.lobpcg_smallest(a, np.array([1.0, -1.0, 1.0]), mg.SolverConfig(k=1))
+    with pytest.raises(mg.InputError):
+        mg.lobpcg_smallest(a, np.ones(3), mg.SolverConfig(k=4))
+
+
+def test_spec_lobpcg_examples(mg):
+    a = mg.SparseSymMatrix.from_coo(3, [0, 1, 2], [0, 1, 2], [1.0, 2.0, 3.0])
+    r = mg.lobpcg_smallest(a, np.ones(3), mg.SolverConfig(k=1))
+    assert r.eigenvalues[0] == pytest.approx(1.0, rel=1e-12)
+    ident = mg.SparseSymMatrix.from_coo(3, [0, 1, 2], [0, 1, 2], [1.0, 1.0, 1.0])
+    r = mg.lobpcg_smallest(ident, np.array([1.0, 2.0, 4.0]), mg.SolverConfig(k=1))
+    assert r.eigenvalues[0] == pytest.approx(0.25, rel=1e-12)
+    assert np.allclose(r.eigenvectors[:, 0], [0, 0, 0.5], atol=1e-8)
+
+
+def test_deflated_q_solve_matches_reference_trajectory(mg, golden_small):
+    """60-iteration best-effort deflated solve (smallest_above_null branch, F2)."""
+    z, meta = golden_small
+    n, ptr, idx, w = graph_from_golden(z, "rand700")
+    g = mg.Graph(n, ptr, idx, w)
+    q = mg.two_hop_laplacian(mg.two_hop_sets(g))
+    cfg = mg.SolverConfig(k=8, tol=1e-6, max_iter=60, seed=42)
+    r = mg.lobpcg_smallest(q, np.ones(n), cfg, deflate=np.full(n, 1 / np.sqrt(n)))
+    assert r.iterations == meta["rand700/q_defl"]["iterations"]
+    ref = z["rand700/q_defl/eigenvalues"]
+    assert np.max(np.abs(r.eigenvalues - ref) / np.abs(ref)) < 1e-10
+    assert np.allclose(r.ritz_sum_history, z["rand700/q_defl/history"], rtol=1e-10)
+
+
+EMBED_CASES = ["path5/embed1", "path5/embed2", "ring6/embed2", "ring9/embed3", "grid4x5/embed3",
+               "path10/embed2", "star4/embed1"] + [f"rand{i}/embed{2 + i % 3}" for i in range(12)]
+
+
+@pytest.mark.parametrize("case", EMBED_CASES)
+def test_embed_small_vs_reference(mg, golden_small, case):
+    z, meta = golden_small
+    name, tag = case.split("/")
+    k = int(tag[len("embed"):])
+    n, ptr, idx, w = graph_from_golden(z, name)
+    cfg = mg.SolverConfig(k=k + 1, tol=1e-8, max_iter=500, seed=42)
+    emb = mg.embed(mg.Graph(n, ptr, idx, w), k, cfg, require_convergence=False)
+    ref = meta[case]["diagnostics"]
+    ev = z[f"{case}/eigenvalues"]
+    assert np.max(np.abs(emb.eigenvalues - ev) / np.maximum(np.abs(ev), 1e-300)) < 1e-8
+    assert emb.diagnostics["epsilon"] == pytest.approx(ref["epsilon"], rel=1e-12)
+    assert emb.diagnostics["mu"] == pytest.approx(ref["mu"], rel=1e-12)
+    assert emb.diagnostics["binding_row"] == ref["binding_row"]
+    assert emb.diagnostics["converged"] == ref["converged"]
+    assert abs(emb.diagnostics["iterations"] - ref["iterations"]) <= 2
+    b = emb.b
+    ang = principal_angles(emb.P, z[f"{case}/P"], b)
+    assert ang.max() < 1e-6
+
+
+def test_embed_disconnected_raises(mg, golden_small):
+    z, _ = golden_small
+    g = mg.Graph(*graph_from_golden(z, "twocomp"))
+    with pytest.raises(mg.DisconnectedGraphError) as e:
+        mg.embed(g, 1)
+    assert e.value.n_components == 2
+    with pytest.raises(mg.InputError):
+        mg.embed(g, 0)
+
+
+def test_embed_raises_convergence_error(mg):
+    from paper_2112_07862_b200 import synthetic
+    g = mg.Graph(*synthetic.random_connected(np.random.default_rng(5), 150, weighted=True))
+    cfg = mg.SolverConfig(k=4, tol=1e-12, max_iter=3)
+    with pytest.raises(mg.ConvergenceError) as e:
+        mg.embed(g, 3, cfg)
+    assert e.value.result is not None and e.value.diagnostics["iterations"] == 3
+
+
+def test_c1_full_pipeline(mg, golden_c1):
+    """Config 1 (N=2000, K=2, fp64, tol 1e-8, 200 iterations)."""
+    z, meta = golden_c1
+    n = meta["graph"]["n"]
+    g = mg.Graph(n, z["graph_ptr"], z["graph_idx"], z["graph_w"])
+    pair = mg.build_operator_pair(g)
+    assert sha(pair.A.indptr) == meta["pair"]["sha_A_ptr"]
+    assert sha(pair.A.indices) == meta["pair"]["sha_A_idx"]
+    assert sha(pair.Q.data) == meta["pair"]["sha_Q_val"]
+    eps_ref = meta["pair"]["eps"]
+    assert abs(pair.epsilon - eps_ref) <= 1e-10 * eps_ref
+    cfg = mg.SolverConfig(k=3, tol=1e-8, max_iter=200, seed=42)
+    emb = mg.embed(g, 2, cfg, require_convergence=False)
+    ev = z["eigenvalues"]
+    assert np.max(np.abs(emb.eigenvalues - ev[1:]) / ev[1:]) < 1e-8
+    assert abs(emb.diagnostics["dropped_eigenvalue"] - ev[0]) < 1e-8 * ev[0]
+    ang = principal_angles(emb.P, z["eigenvectors"][:, 1:], emb.b)
+    assert ang.max() < 1e-6
