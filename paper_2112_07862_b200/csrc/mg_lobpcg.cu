@@ -19,6 +19,7 @@
 //   pass5      X = S Y, P = S[:,k:] Y[k:], and A-images        [255-259]
 // Full re-orthonormalisation (no trusted prefix) every 32 iterations [249].
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <numeric>
 
@@ -312,6 +313,16 @@ __global__ void k_vec_T(int64_t n, const double *__restrict__ x, T *__restrict__
   }
 }
 
+template <typename T>
+__global__ void k_find_nonfinite(const T *__restrict__ x, int64_t n, int ld, int ncols,
+                                 unsigned long long *first) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * ld;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(e % ld);
+    if (c < ncols && !isfinite((double)x[e])) atomicMin(first, (unsigned long long)e);
+  }
+}
+
 // ------------------------------------------------ fused transform + Gram ---
 struct GramSpec {
   int r0 = 0, rw = 0, c0 = 0, cw = 0;
@@ -552,6 +563,8 @@ struct CholArgs {
   double maxnorm0;
   int in0, iw, o0, ow; // M rows physical [in0, in0+iw), cols -> new basis slots [0, ow)
   int use_global;      // matrices in global scratch instead of shared memory
+  double rel_tol;      // relative pivot floor (see blk_cholesky_drop)
+  double abs_tol;      // 1e-12 (eigensolver.py:29) in fp64; fp32 resolution floor in fp32
 };
 
 template <typename T>
@@ -561,7 +574,7 @@ __global__ void __launch_bounds__(kCtrlThreads)
   extern __shared__ __align__(16) double smc[];
   __shared__ int keep[kMaxL];
   __shared__ int rank[kMaxL];
-  __shared__ double dummy;
+  __shared__ double orig[kMaxL];
   const int nl = a.nl, tid = threadIdx.x, nt = blockDim.x;
   double *Gl = a.use_global ? scratch : smc;
   double *R = Gl + nl * nl;
@@ -571,7 +584,8 @@ __global__ void __launch_bounds__(kCtrlThreads)
     Gl[e] = G[(a.order[x] - a.g0) * a.gw + (a.order[y] - a.g0)];
   }
   __syncthreads();
-  int nk = blk_cholesky_drop(Gl, nl, nl, a.maxnorm0, R, nl, keep, &dummy);
+  blk_check_finite(Gl, nl, nl, nl, status + 4, 1);
+  int nk = blk_cholesky_drop(Gl, nl, nl, a.maxnorm0, R, nl, keep, orig, a.rel_tol, a.abs_tol);
   blk_tri_inv_kept(R, nl, nl, keep, Ri, nl);
   if (tid == 0) {
     int r = 0;
@@ -596,6 +610,7 @@ struct RRArgs {
   int m, mp;     // block size, padded
   int want_p;
   int use_global;
+  double rel_tol;
 };
 
 template <typename T>
@@ -611,7 +626,7 @@ __global__ void __launch_bounds__(kCtrlThreads)
   __shared__ double w[kMaxL];
   __shared__ double red[kCtrlThreads];
   __shared__ int cnt;
-  __shared__ double dummy;
+  __shared__ double orig[kMaxL];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int nk = status[0];
   // scratch layout (global): F [hw x smax], HF [hw x smax], (+ big matrices if use_global)
@@ -627,7 +642,9 @@ __global__ void __launch_bounds__(kCtrlThreads)
     W1[e] = G4[x * a.vw + y];
   }
   __syncthreads();
-  int nk2 = blk_cholesky_drop(W1, nk, nk, 0.0, R2, nk, keep, &dummy);
+  blk_check_finite(W1, nk, nk, nk, status + 4, 2);
+  blk_check_finite(H, a.hw, a.hw, a.hw, status + 4, 4);
+  int nk2 = blk_cholesky_drop(W1, nk, nk, 0.0, R2, nk, keep, orig, a.rel_tol);
   blk_tri_inv_kept(R2, nk, nk, keep, W1, nk);  // W1 <- R2^-1
   if (tid == 0) {
     int r = 0;
@@ -676,6 +693,7 @@ __global__ void __launch_bounds__(kCtrlThreads)
     }
   }
   __syncthreads();
+  blk_check_finite(Aj, s, s, s, status + 4, 8);
   blk_jacobi(Aj, s, s, Vj, s, w, cs, pidx, perm, &cnt, red);
   const int take = min(a.m, s);
   for (int i = tid; i < take; i += nt) theta[i] = w[i];
@@ -773,6 +791,7 @@ struct Lobpcg {
       first = false;
       lo += cap;
     } while (lo < total);
+    debug_check(xf ? "tile-pass(transform)" : "tile-pass(gram)");
     double *reds[2] = {red0, red1};
     for (int q = 0; q < ng; ++q) {
       int tot = g[q].rw * g[q].cw;
@@ -788,7 +807,34 @@ struct Lobpcg {
     return s;
   }
 
-  void spmm_cols(int c0, int w) { spmm<T>(ctx, A, S.p + c0, ld, AS.p + c0, ld, w); }
+  void spmm_cols(int c0, int w) {
+    spmm<T>(ctx, A, S.p + c0, ld, AS.p + c0, ld, w);
+    debug_check("spmm");
+  }
+
+  // MG_DEBUG_FINITE=1: locate the first stage that writes a non-finite value
+  int debug_level = -1;
+  int iter_now = 0;
+  void debug_check(const char *stage) {
+    if (debug_level < 0) {
+      const char *e = getenv("MG_DEBUG_FINITE");
+      debug_level = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (!debug_level) return;
+    DBuf<unsigned long long> f(ctx, 1);
+    for (int which = 0; which < 2; ++which) {
+      MG_CUDA(cudaMemsetAsync(f.p, 0xff, sizeof(unsigned long long), ctx->stream));
+      k_find_nonfinite<T><<<grid_for(n * ld, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+          which ? AS.p : S.p, n, ld, 3 * mp + 1, f.p);
+      unsigned long long v;
+      d2h_sync(ctx, &v, f.p, sizeof(v));
+      if (v != ~0ull)
+        throw Error(MG_ERR_INTERNAL, std::string("non-finite in ") + (which ? "AS" : "S") +
+                                         " after " + stage + " at iteration " +
+                                         std::to_string(iter_now) + " row " +
+                                         std::to_string(v / ld) + " col " + std::to_string(v % ld));
+    }
+  }
 
   // per-column reductions: returns host [rn^2 (mp) | qn^2 (mp)]
   void resid(bool write_w, std::vector<double> &out) {
@@ -840,6 +886,9 @@ struct Lobpcg {
     pass(1, 1, 0, 3 * mp, 1, region0, region_w, nullptr, 0, nullptr, nullptr);
   }
 
+  // relative pivot floor: ~sqrt of the storage precision's resolution
+  static double rel_tol() { return sizeof(T) == 8 ? 1e-7 : 1e-3; }
+
   size_t chol_smem(int nl, int &use_global) const {
     size_t need = (size_t)2 * nl * nl * sizeof(double);
     use_global = need > 200 * 1024;
@@ -864,6 +913,8 @@ struct Lobpcg {
     int ug = 0;
     size_t sm = chol_smem(ca.nl, ug);
     ca.use_global = ug;
+    ca.rel_tol = rel_tol();
+    ca.abs_tol = sizeof(T) == 8 ? 1e-12 : 1e-7;
     if (sm > 48 * 1024)
       MG_CUDA(cudaFuncSetAttribute(k_ctrl_chol<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)sm));
@@ -883,6 +934,7 @@ struct Lobpcg {
     int smax = px + vw;
     size_t need = (size_t)2 * std::max(smax * smax, vw * vw) * sizeof(double);
     ra.use_global = need > 200 * 1024;
+    ra.rel_tol = rel_tol();
     size_t sm = ra.use_global ? 0 : need;
     if (sm > 48 * 1024)
       MG_CUDA(cudaFuncSetAttribute(k_ctrl_rr<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -952,13 +1004,18 @@ struct Lobpcg {
     MG_CHECK_LAUNCH(ctx);
     MG_CUDA(cudaMemcpyAsync(colred.p + 2 * mp, theta.p, mp * sizeof(double),
                             cudaMemcpyDeviceToDevice, ctx->stream));
-    MG_CUDA(cudaMemcpyAsync(colred.p + 3 * mp, status.p, 4 * sizeof(int), cudaMemcpyDeviceToDevice,
+    MG_CUDA(cudaMemcpyAsync(colred.p + 3 * mp, status.p, 6 * sizeof(int), cudaMemcpyDeviceToDevice,
                             ctx->stream));
-    std::vector<double> buf(3 * mp + 2);
+    std::vector<double> buf(3 * mp + 3);
     d2h_sync(ctx, buf.data(), colred.p, buf.size() * sizeof(double));
     cr.assign(buf.begin(), buf.begin() + 2 * mp);
     th.assign(buf.begin() + 2 * mp, buf.begin() + 3 * mp);
-    std::memcpy(st, buf.data() + 3 * mp, 4 * sizeof(int));
+    int st6[6];
+    std::memcpy(st6, buf.data() + 3 * mp, 6 * sizeof(int));
+    std::memcpy(st, st6, 4 * sizeof(int));
+    require(st6[4] == 0, MG_ERR_INTERNAL,
+            "non-finite values in the Rayleigh-Ritz / B-Gram matrices (stage mask " +
+                std::to_string(st6[4]) + ")");
   }
 
   SolveResult run(double anorm_in, const double *b_dev, const double *diag_dev, double *eigvecs) {
@@ -1032,7 +1089,9 @@ struct Lobpcg {
     int st[4] = {m, m, m, m};
     int it = 0;
     for (it = 1; it <= sp.max_iter; ++it) {
+      iter_now = it;
       iterate_sync(true, cr, th, st);
+      debug_check("resid");
       if (it > 1 && st[1] < m) {  // basis collapsed last iteration (eigensolver.py:260-266)
         orth_refill_rr(st[1]);
         pcount = 0;
@@ -1052,9 +1111,15 @@ struct Lobpcg {
       for (int c = 0; c < m; ++c)
         if (!cv[c]) vcols.push_back(2 * mp + c);
       deflate_cols(2 * mp, 3 * mp, 2 * mp, mp);
-      spmm_cols(2 * mp, mp);
-      for (int c = 0; c < pcount; ++c) vcols.push_back(mp + c);
       const bool prefix = (it % 32) != 0;
+      if (sizeof(T) == 4 && !prefix) {
+        // fp32: carried A-images drift at fp32 resolution; refresh [AX AP AW]
+        // with one wide SpMM at every full re-orthonormalisation
+        spmm_cols(0, 3 * mp);
+      } else {
+        spmm_cols(2 * mp, mp);
+      }
+      for (int c = 0; c < pcount; ++c) vcols.push_back(mp + c);
       if (prefix) {
         for (int rep = 0; rep < 2; ++rep) {
           if (rep == 0) {

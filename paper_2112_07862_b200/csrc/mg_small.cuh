@@ -17,10 +17,19 @@ namespace mg {
 // G (nl x nl, ld) is overwritten; on exit R holds the upper factor over the
 // logical index space (rows/cols of dropped columns are zero), keep[a] = 1
 // for kept columns.  Returns the kept count (same value in every thread).
+//
+// Gram-based factorisation cannot resolve a column whose post-projection norm
+// is below ~sqrt(eps) of its own norm (the pivot is a cancellation of two
+// nearly equal Gram quantities), so such columns are also dropped: rel_tol
+// bounds pivot / sqrt(G_aa(original)).  This is the only deliberate
+// deviation from the reference's column-sweep MGS, which can keep them; the
+// dropped direction carries < rel_tol of its column.
 __device__ inline int blk_cholesky_drop(double *G, int ld, int nl, double maxnorm0, double *R,
-                                        int ldr, int *keep, double *shared_scalar) {
+                                        int ldr, int *keep, double *orig, double rel_tol,
+                                        double abs_tol = 1e-12) {
   int tid = threadIdx.x, nt = blockDim.x;
   for (int e = tid; e < nl * nl; e += nt) R[(e / nl) * ldr + (e % nl)] = 0.0;
+  for (int a = tid; a < nl; a += nt) orig[a] = G[a * ld + a];
   double maxnorm = maxnorm0;
   int kept = 0;
   __syncthreads();
@@ -28,7 +37,9 @@ __device__ inline int blk_cholesky_drop(double *G, int ld, int nl, double maxnor
     double d = G[a * ld + a];
     double nrm = sqrt(d > 0.0 ? d : 0.0);
     maxnorm = fmax(maxnorm, nrm);
-    bool drop = (nrm == 0.0) || (nrm < 1e-12 * maxnorm);
+    double o = orig[a];
+    bool drop = (nrm == 0.0) || (nrm < abs_tol * maxnorm) ||
+                (nrm < rel_tol * sqrt(o > 0.0 ? o : 0.0));
     if (tid == 0) keep[a] = drop ? 0 : 1;
     if (drop) continue;  // uniform across threads (all read the same G entry)
     ++kept;
@@ -42,7 +53,6 @@ __device__ inline int blk_cholesky_drop(double *G, int ld, int nl, double maxnor
     }
     __syncthreads();
   }
-  (void)shared_scalar;
   __syncthreads();
   return kept;
 }
@@ -172,19 +182,34 @@ __device__ inline void blk_jacobi(double *A, int lda, int n, double *V, int ldv,
     __syncthreads();
     if (c == 0) break;
   }
-  // sort eigenvalues ascending (stable): rank by counting
+  // sort eigenvalues ascending (stable); NaN sorts last so perm is always a
+  // permutation (the caller flags non-finite input separately)
   for (int i = tid; i < n; i += nt) {
     double di = A[i * lda + i];
+    bool ni = di != di;
     int rank = 0;
     for (int j = 0; j < n; ++j) {
       double dj = A[j * lda + j];
-      if (dj < di || (dj == di && j < i)) ++rank;
+      bool nj = dj != dj;
+      bool before = ni ? (nj && j < i) : (nj ? false : (dj < di || (dj == di && j < i)));
+      if (!ni && nj) before = false;
+      if (ni && !nj) before = true;
+      if (before) ++rank;
     }
     perm[rank] = i;
   }
   __syncthreads();
   for (int i = tid; i < n; i += nt) w[i] = A[perm[i] * lda + perm[i]];
   __syncthreads();
+}
+
+// flag (atomicOr into *flag) if any of the n x n entries is not finite
+__device__ inline void blk_check_finite(const double *A, int lda, int rows, int cols, int *flag,
+                                        int bit) {
+  for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+    double v = A[(e / cols) * lda + (e % cols)];
+    if (!isfinite(v)) atomicOr(flag, bit);
+  }
 }
 
 }  // namespace mg
