@@ -59,6 +59,16 @@ int mg_ctx_destroy(mg_ctx *ctx);
 int mg_ctx_set_stream(mg_ctx *ctx, void *stream);
 /* Number of native kernel launches issued through this context so far. */
 int mg_ctx_launch_count(mg_ctx *ctx, int64_t *count /* host */);
+/* The cudaStream_t the context issues work on (for caller-side CUDA events). */
+int mg_ctx_get_stream(mg_ctx *ctx, void **stream /* host */);
+
+/* Hot-kernel timing: when enabled, CUDA events bracket every SpMM / Gram /
+ * update / residual / control launch.  mg_ctx_stats aggregates (and clears)
+ * them per class: counts[c], milliseconds[c], algorithmic bytes[c] for
+ * c = 0 spmm, 1 gram, 2 update, 3 resid, 4 ctrl, 5 setup. */
+int mg_ctx_set_profiling(mg_ctx *ctx, int enable);
+int mg_ctx_stats(mg_ctx *ctx, int64_t *counts /* host 6 */, double *milliseconds /* host 6 */,
+                 double *bytes /* host 6 */);
 
 /* ---- graph-level pieces -------------------------------------------------- */
 /* Graph.connected_components (graph.py:107-123): count + labels numbered by

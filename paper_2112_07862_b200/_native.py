@@ -55,6 +55,9 @@ SIGNATURES = {
     "mg_ctx_destroy": [vp],
     "mg_ctx_set_stream": [vp, vp],
     "mg_ctx_launch_count": [vp, P_i64],
+    "mg_ctx_get_stream": [vp, C.POINTER(vp)],
+    "mg_ctx_set_profiling": [vp, C.c_int],
+    "mg_ctx_stats": [vp, P_i64, P_f64, P_f64],
     "mg_components": [vp, i64, vp, vp, vp, P_i64],
     "mg_laplacian": [vp, i64, vp, vp, vp, vp, vp, vp],
     "mg_two_hop_count": [vp, i64, vp, vp, vp, P_i64],
@@ -141,6 +144,30 @@ def context(device: int = 0):
     call("mg_ctx_create", device, None, C.byref(h))
     _ctx[device] = h
     return h
+
+
+PROF_CLASSES = ("spmm", "gram", "update", "resid", "ctrl", "setup")
+
+
+def stream_handle(device: int = 0) -> int:
+    h = vp()
+    call("mg_ctx_get_stream", context(device), C.byref(h))
+    return int(h.value or 0)
+
+
+def set_profiling(enable: bool, device: int = 0):
+    call("mg_ctx_set_profiling", context(device), int(bool(enable)))
+
+
+def stats(device: int = 0) -> dict:
+    import numpy as np
+    cnt = np.zeros(6, np.int64)
+    ms = np.zeros(6)
+    by = np.zeros(6)
+    call("mg_ctx_stats", context(device), cnt.ctypes.data_as(P_i64), ms.ctypes.data_as(P_f64),
+         by.ctypes.data_as(P_f64))
+    return {name: {"launches": int(cnt[i]), "ms": float(ms[i]), "bytes": float(by[i])}
+            for i, name in enumerate(PROF_CLASSES)}
 
 
 def launch_count(device: int = 0) -> int:

@@ -394,6 +394,11 @@ int mg_ctx_destroy(mg_ctx *ctx) {
   cudaStreamSynchronize(ctx->stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (auto &r : ctx->prof) {
+    cudaEventDestroy(r.start);
+    cudaEventDestroy(r.stop);
+  }
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
   delete ctx;
   MG_API_END
 }
@@ -417,6 +422,39 @@ int mg_ctx_set_stream(mg_ctx *ctx, void *stream) {
 int mg_ctx_launch_count(mg_ctx *ctx, int64_t *count) {
   MG_API_BEGIN(ctx)
   *count = ctx->launches;
+  MG_API_END
+}
+
+int mg_ctx_get_stream(mg_ctx *ctx, void **stream) {
+  MG_API_BEGIN(ctx)
+  *stream = (void *)ctx->stream;
+  MG_API_END
+}
+
+int mg_ctx_set_profiling(mg_ctx *ctx, int enable) {
+  MG_API_BEGIN(ctx)
+  ctx->profiling = enable;
+  MG_API_END
+}
+
+int mg_ctx_stats(mg_ctx *ctx, int64_t *counts, double *milliseconds, double *bytes) {
+  MG_API_BEGIN(ctx)
+  sync(ctx);
+  for (int c = 0; c < PROF_NCLASS; ++c) {
+    counts[c] = 0;
+    milliseconds[c] = 0.0;
+    bytes[c] = 0.0;
+  }
+  for (auto &r : ctx->prof) {
+    float ms = 0.f;
+    MG_CUDA(cudaEventElapsedTime(&ms, r.start, r.stop));
+    counts[r.cls] += 1;
+    milliseconds[r.cls] += ms;
+    bytes[r.cls] += r.bytes;
+    ctx->event_pool.push_back(r.start);
+    ctx->event_pool.push_back(r.stop);
+  }
+  ctx->prof.clear();
   MG_API_END
 }
 

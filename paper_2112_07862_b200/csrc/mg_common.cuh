@@ -48,6 +48,12 @@ inline void require(bool ok, int code, const std::string &msg) {
 }  // namespace mg
 
 // ---------------------------------------------------------------- context ---
+struct mg_prof_rec {
+  int cls;                 // kernel class (mg_prof_class)
+  double bytes;            // algorithmic bytes of this launch
+  cudaEvent_t start, stop;
+};
+
 struct mg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -56,6 +62,9 @@ struct mg_ctx {
   int64_t launches = 0;
   void *pinned = nullptr;       // small pinned staging buffer for D2H scalars
   size_t pinned_bytes = 0;
+  int profiling = 0;            // record CUDA events around hot kernels
+  std::vector<mg_prof_rec> prof;
+  std::vector<cudaEvent_t> event_pool;
 };
 
 namespace mg {
@@ -101,6 +110,16 @@ struct DBuf {
   }
   T *get() const { return p; }
   operator T *() const { return p; }
+};
+
+// Hot-kernel timing (enabled by mg_ctx_set_profiling): events on ctx->stream.
+enum ProfClass { PROF_SPMM = 0, PROF_GRAM = 1, PROF_UPDATE = 2, PROF_RESID = 3, PROF_CTRL = 4,
+                 PROF_SETUP = 5, PROF_NCLASS = 6 };
+struct ProfScope {
+  mg_ctx *ctx;
+  int idx = -1;
+  ProfScope(mg_ctx *c, int cls, double bytes);
+  ~ProfScope();
 };
 
 // Copy device -> host through the context's pinned staging area and wait.

@@ -135,6 +135,10 @@ void spmm(mg_ctx *ctx, const DevCSR<T> &A, const T *X, int ldx, T *Y, int ldy, i
   int G = 32 / L;
   int64_t rows_per_block = 8 * G;
   int grid = grid_for(A.n, (int)rows_per_block, ctx->num_sms * 64);
+  // algorithmic bytes: values+indices, row pointers, X read once, Y written once
+  double bytes = (double)A.nnz * (sizeof(T) + sizeof(int)) + 8.0 * (A.n + 1) +
+                 2.0 * sizeof(T) * (double)A.n * w;
+  ProfScope ps(ctx, PROF_SPMM, bytes);
   k_spmm<T><<<grid, 256, 0, ctx->stream>>>(A.n, A.ptr, A.idx, A.val, X, ldx, Y, ldy, L);
   MG_CHECK_LAUNCH(ctx);
 }
@@ -779,6 +783,9 @@ struct Lobpcg {
     const int cap = kPassThreads * kGT;
     int lo = 0;
     bool first = true;
+    double pbytes = (double)n * ld * sizeof(T) * (a.load_as ? 2 : 1) +
+                    (xf ? (double)n * ow * sizeof(T) * (xf_as ? 2 : 1) : 0.0);
+    ProfScope ps(ctx, xf ? PROF_UPDATE : PROF_GRAM, pbytes);
     do {
       a.tile_lo = lo;
       a.tile_hi = std::min(total, lo + cap);

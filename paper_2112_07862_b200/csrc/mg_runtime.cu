@@ -39,6 +39,33 @@ void h2d(mg_ctx *ctx, void *dev, const void *host, size_t bytes) {
 
 void sync(mg_ctx *ctx) { MG_CUDA(cudaStreamSynchronize(ctx->stream)); }
 
+static cudaEvent_t take_event(mg_ctx *ctx) {
+  if (!ctx->event_pool.empty()) {
+    cudaEvent_t e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  MG_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+ProfScope::ProfScope(mg_ctx *c, int cls, double bytes) : ctx(c) {
+  if (!ctx->profiling) return;
+  mg_prof_rec r;
+  r.cls = cls;
+  r.bytes = bytes;
+  r.start = take_event(ctx);
+  r.stop = take_event(ctx);
+  MG_CUDA(cudaEventRecord(r.start, ctx->stream));
+  idx = (int)ctx->prof.size();
+  ctx->prof.push_back(r);
+}
+
+ProfScope::~ProfScope() {
+  if (idx >= 0) cudaEventRecord(ctx->prof[idx].stop, ctx->stream);
+}
+
 int64_t exclusive_scan_i64(mg_ctx *ctx, const int64_t *counts, int64_t *out, int64_t n) {
   // out has n+1 entries; out[n] = total
   size_t tmp = 0;
