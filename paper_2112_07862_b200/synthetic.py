@@ -34,15 +34,15 @@ class Config:
 # BASELINE.json "configs" (max_iter is not stated for C2-C5; SURVEY 8(d) asks
 # for an explicit value -- the default 500 does not converge C2, F4).
 CONFIGS = {
-    "c1": Config("c1", 2_000, 10, 2, 1e-8, 200, "f64",
+    "c1": Config("c1", 2_000, 10, 2, 1e-8, 200, "fp64",
                  "uniform unit square 2-D, kNN k=10, K=2, fp64, tol 1e-8, 200 it"),
-    "c2": Config("c2", 100_000, 10, 4, 1e-6, 3000, "f64",
+    "c2": Config("c2", 100_000, 10, 4, 1e-6, 3000, "fp64",
                  "Swiss roll N=100K, kNN k=10, K=4, tol 1e-6"),
-    "c3": Config("c3", 1_000_000, 12, 8, 1e-5, 3000, "f32",
+    "c3": Config("c3", 1_000_000, 12, 8, 1e-5, 3000, "fp32",
                  "unit sphere S^2 N=1M, kNN k=12, K=8, fp32 + fp64 Gram, tol 1e-5"),
-    "c4": Config("c4", 5_000_000, 10, 16, 1e-5, 3000, "f32",
+    "c4": Config("c4", 5_000_000, 10, 16, 1e-5, 3000, "fp32",
                  "10 disjoint unit squares x 500K, kNN k=10, K=16, fp32, tol 1e-5"),
-    "c5": Config("c5", 20_000_000, 8, 32, 1e-4, 3000, "f32",
+    "c5": Config("c5", 20_000_000, 8, 32, 1e-4, 3000, "fp32",
                  "unit cube 3-D N=20M, kNN k=8, K=32, fp32 + fp64 Gram, tol 1e-4"),
 }
 
