@@ -187,6 +187,7 @@ typedef struct mg_embed_diag {
   int64_t binding_row, q_nnz, a_nnz, t_nnz, n_components;
   int32_t iterations, eps_iterations;
   double seconds_setup, seconds_eps, seconds_solve;
+  int64_t fast_steps, fast_fallbacks;   /* single-Gram-pass iterations / fallbacks */
 } mg_embed_diag;
 
 /* embed (embedding.py:77-103): components check, build_operator_pair,

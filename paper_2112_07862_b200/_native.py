@@ -45,7 +45,8 @@ class EmbedDiag(C.Structure):
                 ("dropped_eigenvalue", f64), ("generalized_degree", f64),
                 ("binding_row", i64), ("q_nnz", i64), ("a_nnz", i64), ("t_nnz", i64),
                 ("n_components", i64), ("iterations", i32), ("eps_iterations", i32),
-                ("seconds_setup", f64), ("seconds_eps", f64), ("seconds_solve", f64)]
+                ("seconds_setup", f64), ("seconds_eps", f64), ("seconds_solve", f64),
+                ("fast_steps", i64), ("fast_fallbacks", i64)]
 
 
 # name -> argtypes (restype is always c_int status, except mg_last_error / mg_version)

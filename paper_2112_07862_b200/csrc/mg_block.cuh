@@ -60,6 +60,7 @@ struct SolveResult {
   std::vector<int> converged;
   int iterations = 0;
   int64_t normals_used = 0;
+  int64_t fast_steps = 0, fast_fallbacks = 0;
 };
 
 // lobpcg_smallest on (A, diag(b)); eigvecs: device n x k double row-major in

@@ -300,6 +300,8 @@ static int embed_impl(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t 
   sync(ctx);
   double t4 = now_s();
   d.iterations = r.iterations;
+  d.fast_steps = r.fast_steps;
+  d.fast_fallbacks = r.fast_fallbacks;
   d.dropped_eigenvalue = r.eigenvalues[0];
   d.seconds_setup = (t1 - t0) + (t3 - t2);
   d.seconds_eps = t2 - t1;

@@ -1,0 +1,583 @@
+// Fast-path LOBPCG kernels (prefix iterations):
+//   k_gram2         one read of S = [X P W] and AS -> G_B = S'BS and G_A = S'AS
+//   k_ctrl_fast     two-pass projection + Cholesky (drop rule) + Rayleigh-Ritz
+//                   entirely on the small Gram matrices (one thread block)
+//   k_update_resid  P = S Zp, X = X Yx + P (and A-images), then the next
+//                   residual block W = dinv (AX - B X Theta) and its norms
+// Row tiles of S/AS are staged with 1-D bulk async copies (cp.async.bulk +
+// mbarrier complete_tx) into a shared-memory ring.
+#pragma once
+#include "mg_block.cuh"
+#include "mg_small.cuh"
+
+namespace mg {
+
+static constexpr int kFTK = 32;      // rows per tile
+static constexpr int kMaxFast = 256;
+static constexpr int kFThreads = 256;
+
+// ------------------------------------------------------- bulk copy helpers ---
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// issue the copies of row tile `tile` (rows [tile*TK, ...)) into ring stage st
+template <typename T>
+__device__ __forceinline__ void issue_tile(const T *S, const T *AS, const T *b, int64_t n, int ld,
+                                           int64_t tile, T *sS, T *sA, T *sb, uint64_t *bar) {
+  int64_t r0 = tile * kFTK;
+  int nr = (int)min((int64_t)kFTK, n - r0);
+  uint32_t bytes_m = (uint32_t)(nr * ld * sizeof(T));
+  uint32_t bytes_b = (uint32_t)(((nr * sizeof(T)) + 15) / 16 * 16);
+  uint32_t total = bytes_m * (AS ? 2 : 1) + (b ? bytes_b : 0);
+  mbar_expect_tx(bar, total);
+  bulk_g2s(sS, S + r0 * ld, bytes_m, bar);
+  if (AS) bulk_g2s(sA, AS + r0 * ld, bytes_m, bar);
+  if (b) bulk_g2s(sb, b + r0, bytes_b, bar);
+}
+
+// ------------------------------------------------------------- k_gram2 ---
+// Thread layout: nbr Gram blocks (8x8) in this round; groups of nbr threads
+// split the rows of each tile (row r -> group r % G).  fp32 data: products
+// accumulate in fp32 over a few tiles, then flush into fp64 (shared memory);
+// fp64 data accumulates in fp64 registers.
+struct Gram2Args {
+  int64_t n;
+  int ld, w, nb;          // w columns [0, w), nb = ceil(w/8) blocks per side
+  int blk_lo, nbr;        // Gram blocks [blk_lo, blk_lo + nbr) of the enumeration
+  int nsym;               // blocks per Gram: nb*(nb+1)/2
+  double *part;           // [grid][2][w*w] (only computed block entries written)
+};
+
+__device__ __forceinline__ void gram2_decode(int blk, int nb, int nsym, int &g, int &bi, int &bj) {
+  g = blk >= nsym ? 1 : 0;
+  int t = blk - g * nsym;
+  int r = 0;
+  while (t >= nb - r) {
+    t -= nb - r;
+    ++r;
+  }
+  bi = r;
+  bj = r + t;
+}
+
+template <typename T, int NS>
+__global__ void __launch_bounds__(kFThreads, 1)
+    k_gram2(const T *__restrict__ S, const T *__restrict__ AS, const T *__restrict__ b,
+            Gram2Args a) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr bool F32 = sizeof(T) == 4;
+  const int ld = a.ld;
+  const size_t tile_elems = (size_t)kFTK * ld + 16;
+  T *ring = reinterpret_cast<T *>(smraw);
+  // stage s: S tile, AS tile, b tile
+  auto stS = [&](int s) { return ring + (size_t)s * (2 * tile_elems + kFTK + 16); };
+  auto stA = [&](int s) { return stS(s) + tile_elems; };
+  auto stB = [&](int s) { return stS(s) + 2 * tile_elems; };
+  unsigned char *after = smraw + (size_t)NS * (2 * tile_elems + kFTK + 16) * sizeof(T);
+  after = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(after) + 15) & ~uintptr_t(15));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(after);
+  double *acc64 = reinterpret_cast<double *>(after + 64);  // [64][kFThreads]
+
+  const int tid = threadIdx.x;
+  const int G = max(1, kFThreads / a.nbr);
+  const int grp = tid / a.nbr, blk = tid - grp * a.nbr;
+  const bool active = grp < G;
+  int g = 0, bi = 0, bj = 0;
+  if (active) gram2_decode(a.blk_lo + blk, a.nb, a.nsym, g, bi, bj);
+
+  const int64_t ntiles = (a.n + kFTK - 1) / kFTK;
+  const int64_t t_begin = ntiles * blockIdx.x / gridDim.x;
+  const int64_t t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    fence_proxy_async();
+  }
+  if (F32)
+    for (int e = tid; e < 64 * kFThreads; e += kFThreads) acc64[e] = 0.0;
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < NS && t_begin + s < t_end; ++s)
+      issue_tile(S, AS, b, a.n, ld, t_begin + s, stS(s), stA(s), stB(s), &bars[s]);
+
+  float accf[64];
+  double accd[F32 ? 1 : 64];
+#pragma unroll
+  for (int e = 0; e < 64; ++e) accf[e] = 0.f;
+  if (!F32) {
+#pragma unroll
+    for (int e = 0; e < (F32 ? 1 : 64); ++e) accd[e] = 0.0;
+  }
+  int since_flush = 0;
+  for (int64_t t = t_begin; t < t_end; ++t) {
+    const int s = (int)((t - t_begin) % NS);
+    const uint32_t phase = (uint32_t)(((t - t_begin) / NS) & 1);
+    mbar_wait(&bars[s], phase);
+    const int nr = (int)min((int64_t)kFTK, a.n - t * kFTK);
+    if (active) {
+      const T *U = stS(s) + bi * 8;
+      const T *Vb = (g == 0 ? stS(s) : stA(s)) + bj * 8;
+      const T *bb = stB(s);
+      for (int r = grp; r < nr; r += G) {
+        T u[8], v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          u[q] = U[r * ld + q];
+          v[q] = Vb[r * ld + q];
+        }
+        if (g == 0) {
+          const T wr = bb[r];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = wr * v[q];
+        }
+        if (F32) {
+#pragma unroll
+          for (int x = 0; x < 8; ++x)
+#pragma unroll
+            for (int y = 0; y < 8; ++y) accf[x * 8 + y] = fmaf((float)u[x], (float)v[y], accf[x * 8 + y]);
+        } else {
+#pragma unroll
+          for (int x = 0; x < 8; ++x)
+#pragma unroll
+            for (int y = 0; y < 8; ++y)
+              accd[(x * 8 + y) % (F32 ? 1 : 64)] =
+                  fma((double)u[x], (double)v[y], accd[(x * 8 + y) % (F32 ? 1 : 64)]);
+        }
+      }
+    }
+    __syncthreads();  // everyone is done with stage s
+    if (tid == 0 && t + NS < t_end) {
+      fence_proxy_async();
+      issue_tile(S, AS, b, a.n, ld, t + NS, stS(s), stA(s), stB(s), &bars[s]);
+    }
+    if (F32 && ++since_flush == 1) {
+      since_flush = 0;
+      if (active) {
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          acc64[e * kFThreads + tid] += (double)accf[e];
+          accf[e] = 0.f;
+        }
+      }
+    }
+  }
+  if (F32) {
+    if (active) {
+#pragma unroll
+      for (int e = 0; e < 64; ++e) acc64[e * kFThreads + tid] += (double)accf[e];
+    }
+  } else {
+    if (active) {
+#pragma unroll
+      for (int e = 0; e < (F32 ? 1 : 64); ++e) acc64[e * kFThreads + tid] = accd[e];
+    }
+  }
+  __syncthreads();
+  // reduce the row groups (fixed order) and write this CTA's partial Grams
+  const int w = a.w;
+  double *dst = a.part + (size_t)blockIdx.x * 2 * w * w;
+  for (int item = tid; item < a.nbr * 64; item += kFThreads) {
+    const int bk = item / 64, e = item - bk * 64;
+    double sum = 0.0;
+    for (int q = 0; q < G; ++q) sum += acc64[e * kFThreads + q * a.nbr + bk];
+    int gg, ii, jj;
+    gram2_decode(a.blk_lo + bk, a.nb, a.nsym, gg, ii, jj);
+    const int i = ii * 8 + (e >> 3), j = jj * 8 + (e & 7);
+    if (i < w && j < w) dst[(size_t)gg * w * w + i * w + j] = sum;
+  }
+}
+
+// sum CTA partials (fixed order) and mirror the symmetric lower blocks
+__global__ void k_reduce_gram2(const double *__restrict__ part, int nb_cta, int w,
+                               double *__restrict__ GB, double *__restrict__ GA) {
+  const int tot = 2 * w * w;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
+    const int g = e / (w * w);
+    const int r = e - g * w * w;
+    int i = r / w, j = r - i * w;
+    if ((i >> 3) > (j >> 3)) {
+      int t = i;
+      i = j;
+      j = t;
+    }
+    const size_t src = (size_t)g * w * w + i * w + j;
+    double s = 0.0;
+    for (int q = 0; q < nb_cta; ++q) s += part[(size_t)q * tot + src];
+    (g ? GA : GB)[r] = s;
+  }
+}
+
+// -------------------------------------------------------- k_update_resid ---
+// P_new = S[:, 0:w] Zp ; X_new = S[:, 0:mp] Yx + P_new (same for AS);
+// W = dinv (AX_new - b X_new theta);  partial column sums of R^2 and X^2.
+// M layout (T, row-major): Zp [w x mp] then Yx [mp x mp].
+struct UpdArgs {
+  int64_t n;
+  int ld, w, m, mp;
+  const int *skip;        // device flag: nonzero -> return (fallback iteration)
+  double *part;           // [grid][2*mp]
+};
+
+template <typename T, int NS>
+__global__ void __launch_bounds__(kFThreads, 1)
+    k_update_resid(T *__restrict__ S, T *__restrict__ AS, const T *__restrict__ b,
+                   const T *__restrict__ prec, const T *__restrict__ Mg,
+                   const double *__restrict__ theta, UpdArgs a) {
+  if (*a.skip) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int ld = a.ld, w = a.w, mp = a.mp;
+  const size_t tile_elems = (size_t)kFTK * ld + 16;
+  T *ring = reinterpret_cast<T *>(smraw);
+  auto stS = [&](int s) { return ring + (size_t)s * (2 * tile_elems + kFTK + 16); };
+  auto stA = [&](int s) { return stS(s) + tile_elems; };
+  auto stB = [&](int s) { return stS(s) + 2 * tile_elems; };
+  T *sM = ring + (size_t)NS * (2 * tile_elems + kFTK + 16);   // Zp then Yx
+  const int mlen = w * mp + mp * mp;
+  T *oPS = sM + mlen + 16;                                     // [TK][mp] each
+  T *oPA = oPS + kFTK * mp;
+  T *oXS = oPA + kFTK * mp;
+  T *oXA = oXS + kFTK * mp;
+  T *sth = oXA + kFTK * mp;                                    // theta (mp)
+  T *sprec = sth + mp + 4;                                     // prec tile (TK)
+  unsigned char *after = reinterpret_cast<unsigned char *>(sprec + kFTK + 4);
+  after = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(after) + 15) & ~uintptr_t(15));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(after);
+  double *red = reinterpret_cast<double *>(after + 64);       // [kFThreads][2]
+
+  const int tid = threadIdx.x;
+  for (int e = tid; e < mlen; e += kFThreads) sM[e] = Mg[e];
+  for (int e = tid; e < mp; e += kFThreads) sth[e] = e < a.m ? (T)theta[e] : T(0);
+  const int64_t ntiles = (a.n + kFTK - 1) / kFTK;
+  const int64_t t_begin = ntiles * blockIdx.x / gridDim.x;
+  const int64_t t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    fence_proxy_async();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < NS && t_begin + s < t_end; ++s)
+      issue_tile<T>(S, AS, b, a.n, ld, t_begin + s, stS(s), stA(s), stB(s), &bars[s]);
+
+  // residual norm accumulators: thread owns column (tid % mp) for rows tid/mp + k*R
+  const int R = kFThreads / mp;
+  const int rc = tid % mp, rrow = tid / mp;
+  double sr = 0.0, sx = 0.0;
+  const T *Zp = sM, *Yx = sM + w * mp;
+  // output tiles: (8 rows x 4 cols) register blocks over [TK x mp] per matrix
+  const int cb = (mp + 3) / 4, nblk = (kFTK / 8) * cb;  // per matrix
+  for (int64_t t = t_begin; t < t_end; ++t) {
+    const int s = (int)((t - t_begin) % NS);
+    const uint32_t phase = (uint32_t)(((t - t_begin) / NS) & 1);
+    mbar_wait(&bars[s], phase);
+    const int64_t r0 = t * kFTK;
+    const int nr = (int)min((int64_t)kFTK, a.n - r0);
+    for (int e = tid; e < kFTK; e += kFThreads) sprec[e] = (e < nr && prec) ? prec[r0 + e] : T(1);
+    // P_new for S and AS
+    for (int job = tid; job < 2 * nblk; job += kFThreads) {
+      const int mat = job / nblk, jb = job - mat * nblk;
+      const int rb = jb / cb, c0 = (jb - rb * cb) * 4;
+      const T *src = (mat ? stA(s) : stS(s)) + rb * 8 * ld;
+      T acc[8][4];
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = T(0);
+      for (int k = 0; k < w; ++k) {
+        T mz[4];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) mz[y] = Zp[k * mp + c0 + y];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          const T u = src[x * ld + k];
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] += u * mz[y];
+        }
+      }
+      T *dst = (mat ? oPA : oPS) + rb * 8 * mp + c0;
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+          if (c0 + y < mp) dst[x * mp + y] = acc[x][y];
+    }
+    __syncthreads();
+    // X_new = X Yx + P_new
+    for (int job = tid; job < 2 * nblk; job += kFThreads) {
+      const int mat = job / nblk, jb = job - mat * nblk;
+      const int rb = jb / cb, c0 = (jb - rb * cb) * 4;
+      const T *src = (mat ? stA(s) : stS(s)) + rb * 8 * ld;
+      const T *pn = (mat ? oPA : oPS) + rb * 8 * mp + c0;
+      T acc[8][4];
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = (c0 + y < mp) ? pn[x * mp + y] : T(0);
+      for (int k = 0; k < mp; ++k) {
+        T my[4];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) my[y] = Yx[k * mp + c0 + y];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          const T u = src[x * ld + k];
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] += u * my[y];
+        }
+      }
+      T *dst = (mat ? oXA : oXS) + rb * 8 * mp + c0;
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+          if (c0 + y < mp) dst[x * mp + y] = acc[x][y];
+    }
+    __syncthreads();
+    // residual + W, and write back [X P W] / [AX AP] rows
+    for (int rr = rrow; rr < nr && rrow < R; rr += R) {
+      const T x = oXS[rr * mp + rc];
+      const T ax = oXA[rr * mp + rc];
+      T wv = T(0);
+      if (rc < a.m) {
+        const T bx = stB(s)[rr] * x;
+        const T r = ax - bx * sth[rc];
+        sr += (double)r * (double)r;
+        sx += (double)x * (double)x;
+        wv = sprec[rr] * r;
+      }
+      T *srow = S + (r0 + rr) * ld;
+      T *arow = AS + (r0 + rr) * ld;
+      srow[rc] = x;
+      srow[mp + rc] = oPS[rr * mp + rc];
+      srow[2 * mp + rc] = wv;
+      arow[rc] = ax;
+      arow[mp + rc] = oPA[rr * mp + rc];
+    }
+    __syncthreads();  // stage s and the output tiles are free
+    if (tid == 0 && t + NS < t_end) {
+      fence_proxy_async();
+      issue_tile<T>(S, AS, b, a.n, ld, t + NS, stS(s), stA(s), stB(s), &bars[s]);
+    }
+  }
+  red[tid * 2] = (rrow < R) ? sr : 0.0;
+  red[tid * 2 + 1] = (rrow < R) ? sx : 0.0;
+  __syncthreads();
+  for (int c = tid; c < 2 * mp; c += kFThreads) {
+    const int col = c % mp, which = c / mp;
+    double s2 = 0.0;
+    for (int q = 0; q < R; ++q) s2 += red[(q * mp + col) * 2 + which];
+    a.part[(size_t)blockIdx.x * 2 * mp + c] = s2;
+  }
+}
+
+// ---------------------------------------------------------- k_ctrl_fast ---
+// Small-matrix LOBPCG step for a prefix iteration.  G_B / G_A are w x w over
+// physical columns [0, w) = [X | P | W].  Logical basis: X (m trusted
+// columns), then V = (active W, valid P) in the reference's order.
+//   X~ = X RX^-1 with RX = chol(G_XX)       (X re-orthonormalised every step)
+//   C  = X~'BV, D = RX^-1 C                 (projection, eigensolver.py:126-129)
+//   Gv = G_VV - C'C                         (B-Gram of V - X~ C)
+//   Cholesky with the drop rule on Gv       (eigensolver.py:133-152)
+//   T  = [[I, -D Rinv], [0, Rinv]];  G_RR = T' G_A T;  eigh (Jacobi)
+// Fallback flag when any kept column's pivot^2 < fast_tol * (its un-projected
+// B-norm^2): the multi-pass path then materialises the projections instead.
+struct FastArgs {
+  int m, mp, w;
+  int nv;
+  int vcols[kMaxFast];    // physical columns of V in logical order
+  double fast_tol;
+  double rel_tol, abs_tol;
+  int use_global;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(512)
+    k_ctrl_fast(FastArgs a, const double *__restrict__ GB, const double *__restrict__ GA,
+                T *__restrict__ Mout, double *__restrict__ theta, int *status, double *scratch) {
+  extern __shared__ __align__(16) double smf[];
+  __shared__ int keep[kMaxFast];
+  __shared__ int rank[kMaxFast];
+  __shared__ int perm[kMaxFast];
+  __shared__ int pidx[kMaxFast + 2];
+  __shared__ double cs[kMaxFast + 2];
+  __shared__ double wv[kMaxFast];
+  __shared__ double orig[kMaxFast];
+  __shared__ double unproj[kMaxFast];
+  __shared__ double red[512];
+  __shared__ int cnt, bad;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int m = a.m, nv = a.nv, w = a.w, mp = a.mp;
+  // global scratch: C, D [m x nv]; RX, RXi [m x m]; T, HT [w x smax]
+  double *C = scratch;
+  double *D = C + m * nv;
+  double *RX = D + m * nv;
+  double *RXi = RX + m * m;
+  double *GX = RXi + m * m;
+  const int smax = m + nv;
+  double *Tm = GX + m * m;
+  double *HT = Tm + (size_t)w * smax;
+  double *big = HT + (size_t)w * smax;
+  double *Gv = a.use_global ? big : smf;
+  double *R = Gv + nv * nv;
+  if (tid == 0) bad = 0;
+  // X is re-orthonormalised from its own B-Gram every step (X~ = X RX^-1), so
+  // single-pass rounding in the previous update never accumulates
+  for (int e = tid; e < m * m; e += nt) GX[e] = GB[(e / m) * w + (e % m)];
+  __syncthreads();
+  const int nkx = blk_cholesky_drop(GX, m, m, 0.0, RX, m, keep, orig, 1e-6, 1e-300);
+  if (nkx < m) {
+    if (tid == 0) status[5] = 1;
+    return;
+  }
+  blk_tri_inv_kept(RX, m, m, keep, RXi, m);
+  for (int e = tid; e < m * nv; e += nt) {  // C = RX^-T G_XV
+    int x = e / nv, q = e - x * nv;
+    double s2 = 0.0;
+    for (int y = 0; y <= x; ++y) s2 += RXi[y * m + x] * GB[y * w + a.vcols[q]];
+    C[e] = s2;
+  }
+  __syncthreads();
+  for (int e = tid; e < m * nv; e += nt) {  // D = RX^-1 C  (X coefficients of the projection)
+    int x = e / nv, q = e - x * nv;
+    double s2 = 0.0;
+    for (int y = x; y < m; ++y) s2 += RXi[x * m + y] * C[y * nv + q];
+    D[e] = s2;
+  }
+  for (int e = tid; e < nv * nv; e += nt) {  // Gv = G_VV - C'C
+    int p = e / nv, q = e - p * nv;
+    double s2 = GB[a.vcols[p] * w + a.vcols[q]];
+    for (int x = 0; x < m; ++x) s2 -= C[x * nv + p] * C[x * nv + q];
+    Gv[e] = s2;
+    if (p == q) unproj[p] = GB[a.vcols[p] * w + a.vcols[p]];
+  }
+  __syncthreads();
+  blk_check_finite(Gv, nv, nv, nv, status + 4, 16);
+  const int nk = blk_cholesky_drop(Gv, nv, nv, 1.0, R, nv, keep, orig, a.rel_tol, a.abs_tol);
+  // quality: every kept pivot must be resolvable from the Gram at this precision
+  for (int q = tid; q < nv; q += nt)
+    if (keep[q]) {
+      double piv = R[q * nv + q];
+      if (!(piv * piv >= a.fast_tol * unproj[q])) atomicOr(&bad, 1);
+    }
+  __syncthreads();
+  if (bad) {
+    if (tid == 0) status[5] = 1;
+    return;
+  }
+  blk_tri_inv_kept(R, nv, nv, keep, Gv, nv);  // Gv <- Rinv
+  if (tid == 0) {
+    int r = 0;
+    for (int t = 0; t < nv; ++t) rank[t] = keep[t] ? r++ : -1;
+  }
+  __syncthreads();
+  const int s = m + nk;
+  for (int e = tid; e < w * s; e += nt) Tm[e] = 0.0;
+  __syncthreads();
+  for (int e = tid; e < m * m; e += nt) Tm[(e / m) * s + (e % m)] = RXi[e];
+  for (int e = tid; e < nv * nv; e += nt) {
+    int p = e / nv, t = e - p * nv;
+    if (keep[t] && keep[p] && p <= t) Tm[a.vcols[p] * s + m + rank[t]] = Gv[p * nv + t];
+  }
+  for (int e = tid; e < m * nv; e += nt) {  // X rows: -D Rinv
+    int x = e / nv, t = e - x * nv;
+    if (!keep[t]) continue;
+    double s2 = 0.0;
+    for (int p = 0; p <= t; ++p)
+      if (keep[p]) s2 += D[x * nv + p] * Gv[p * nv + t];
+    Tm[x * s + m + rank[t]] = -s2;
+  }
+  __syncthreads();
+  for (int e = tid; e < w * s; e += nt) {  // HT = G_A T
+    int i = e / s, j = e - i * s;
+    double s2 = 0.0;
+    for (int u = 0; u < w; ++u) {
+      double tv = Tm[u * s + j];
+      if (tv != 0.0) s2 += GA[i * w + u] * tv;
+    }
+    HT[e] = s2;
+  }
+  __syncthreads();
+  double *Aj = a.use_global ? big + 2 * nv * nv : smf;
+  double *Vj = Aj + s * s;
+  for (int e = tid; e < s * s; e += nt) {
+    int i = e / s, j = e - i * s;
+    double s2 = 0.0;
+    for (int u = 0; u < w; ++u) {
+      double tv = Tm[u * s + i];
+      if (tv != 0.0) s2 += tv * HT[u * s + j];
+    }
+    Aj[e] = s2;
+  }
+  __syncthreads();
+  for (int e = tid; e < s * s; e += nt) {
+    int i = e / s, j = e - i * s;
+    if (i < j) {
+      double v = 0.5 * (Aj[i * s + j] + Aj[j * s + i]);
+      Aj[i * s + j] = v;
+      Aj[j * s + i] = v;
+    }
+  }
+  __syncthreads();
+  blk_check_finite(Aj, s, s, s, status + 4, 8);
+  blk_jacobi(Aj, s, s, Vj, s, wv, cs, pidx, perm, &cnt, red);
+  const int take = min(m, s);
+  for (int i = tid; i < take; i += nt) theta[i] = wv[i];
+  // Zp [w x mp] = T[:, m:s] Y[m:s, :take];  Yx [mp x mp] = Y[0:m, :take]
+  for (int e = tid; e < w * mp; e += nt) {
+    int r = e / mp, c = e - r * mp;
+    double s2 = 0.0;
+    if (c < take) {
+      int col = perm[c];
+      for (int u = m; u < s; ++u) s2 += Tm[r * s + u] * Vj[u * s + col];
+    }
+    Mout[e] = (T)s2;
+  }
+  for (int e = tid; e < mp * mp; e += nt) {  // Yx = RX^-1 Y[0:m, :take]
+    int x = e / mp, c = e - x * mp;
+    double v = 0.0;
+    if (x < m && c < take) {
+      int col = perm[c];
+      for (int y = x; y < m; ++y) v += RXi[x * m + y] * Vj[y * s + col];
+    }
+    Mout[w * mp + e] = (T)v;
+  }
+  if (tid == 0) {
+    status[0] = nk;
+    status[1] = take;
+    status[2] = nk;
+    status[3] = s;
+    status[5] = 0;
+  }
+}
+
+}  // namespace mg

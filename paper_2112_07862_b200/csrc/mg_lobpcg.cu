@@ -26,6 +26,7 @@
 #include "mg_block.cuh"
 #include "mg_graph.cuh"
 #include "mg_small.cuh"
+#include "mg_fastk.cuh"
 
 namespace mg {
 
@@ -894,7 +895,14 @@ struct Lobpcg {
   }
 
   // relative pivot floor: ~sqrt of the storage precision's resolution
-  static double rel_tol() { return sizeof(T) == 8 ? 1e-7 : 1e-3; }
+  static double env_double(const char *name, double dflt) {
+    const char *e = getenv(name);
+    return e ? atof(e) : dflt;
+  }
+  static double rel_tol() { return sizeof(T) == 8 ? 1e-7 : env_double("MG_REL_TOL32", 1e-2); }
+  // fp32: carried A-images drift ~1e-7 per transform and small pivots amplify
+  // it, so [AX AP AW] is recomputed by one wide SpMM every `refresh` steps
+  int refresh_period() const { return sizeof(T) == 8 ? 32 : (int)env_double("MG_REFRESH32", 16); }
 
   size_t chol_smem(int nl, int &use_global) const {
     size_t need = (size_t)2 * nl * nl * sizeof(double);
@@ -1025,6 +1033,145 @@ struct Lobpcg {
                 std::to_string(st6[4]) + ")");
   }
 
+  // ---- fast path (prefix iterations): one Gram pass + fused update/residual
+  bool fast_ok = false;
+  int grid_fast = 0;
+  size_t gram2_smem = 0, upd_smem = 0, fast_smem = 0;
+  int fast_global = 0;
+  DBuf<double> gpart;
+  int64_t fast_steps = 0, fast_fallbacks = 0;
+
+  void fast_setup() {
+    const char *env = getenv("MG_FAST");
+    if (env && env[0] == '0') return;
+    const int w = 3 * mp;
+    const size_t tile_elems = (size_t)kFTK * ld + 16;
+    const size_t stage = (2 * tile_elems + kFTK + 16) * sizeof(T);
+    gram2_smem = 3 * stage + 64 + 64 + (size_t)64 * kFThreads * sizeof(double) + 128;
+    const size_t mlen = (size_t)w * mp + (size_t)mp * mp;
+    upd_smem = 2 * stage + (mlen + 16 + 4 * kFTK * mp + mp + 4 + kFTK + 4) * sizeof(T) + 64 + 64 +
+               (size_t)kFThreads * 2 * sizeof(double) + 128;
+    if (gram2_smem > 225 * 1024 || upd_smem > 225 * 1024 || m > 64) return;
+    int smax = m + 2 * m;
+    size_t need = (size_t)2 * std::max(smax * smax, 4 * m * m) * sizeof(double);
+    fast_global = need > 190 * 1024;
+    fast_smem = fast_global ? 0 : need;
+    MG_CUDA(cudaFuncSetAttribute(k_gram2<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)gram2_smem));
+    MG_CUDA(cudaFuncSetAttribute(k_update_resid<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)upd_smem));
+    if (fast_smem > 48 * 1024)
+      MG_CUDA(cudaFuncSetAttribute(k_ctrl_fast<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)fast_smem));
+    int64_t ntile = (n + kFTK - 1) / kFTK;
+    grid_fast = (int)std::min<int64_t>(ntile, ctx->num_sms);
+    gpart.alloc(ctx, (size_t)grid_fast * 2 * w * w);
+    fast_ok = true;
+  }
+
+  // returns false when the small-matrix quality check asks for the multi-pass path
+  bool fast_iteration(const std::vector<int> &vcols, std::vector<double> &cr,
+                      std::vector<double> &th, int st[4]) {
+    const int w = 3 * mp;
+    Gram2Args ga{};
+    ga.n = n;
+    ga.ld = ld;
+    ga.w = w;
+    ga.nb = (w + 7) / 8;
+    ga.nsym = ga.nb * (ga.nb + 1) / 2;
+    ga.part = gpart.p;
+    const int total = 2 * ga.nsym;
+    {
+      ProfScope ps(ctx, PROF_GRAM, 2.0 * n * ld * sizeof(T));
+      for (int lo = 0; lo < total; lo += kFThreads) {
+        ga.blk_lo = lo;
+        ga.nbr = std::min(kFThreads, total - lo);
+        k_gram2<T, 3><<<grid_fast, kFThreads, gram2_smem, ctx->stream>>>(S.p, AS.p, bw.p, ga);
+        MG_CHECK_LAUNCH(ctx);
+      }
+    }
+    k_reduce_gram2<<<grid_for(2 * w * w, 256, 4 * ctx->num_sms), 256, 0, ctx->stream>>>(
+        gpart.p, grid_fast, w, Gr0.p, Gr1.p);
+    MG_CHECK_LAUNCH(ctx);
+    FastArgs fa{};
+    fa.m = m;
+    fa.mp = mp;
+    fa.w = w;
+    fa.nv = (int)vcols.size();
+    require(fa.nv <= kMaxFast, MG_ERR_INTERNAL, "fast path: too many columns");
+    for (int i = 0; i < fa.nv; ++i) fa.vcols[i] = vcols[i];
+    // pivot^2 / unprojected norm^2 floor: below it the single-pass basis
+    // S*T loses more than ~1e-11 (fp64) / ~6e-5 (fp32) of B-orthonormality
+    fa.fast_tol = sizeof(T) == 8 ? 1e-10 : env_double("MG_FAST_TOL32", 1e-4);
+    fa.rel_tol = rel_tol();
+    fa.abs_tol = sizeof(T) == 8 ? 1e-12 : 1e-7;
+    fa.use_global = fast_global;
+    {
+      ProfScope ps(ctx, PROF_CTRL, 0.0);
+      k_ctrl_fast<T><<<1, 512, fast_smem, ctx->stream>>>(fa, Gr0.p, Gr1.p, M.p, theta.p, status.p,
+                                                         scratch.p);
+      MG_CHECK_LAUNCH(ctx);
+    }
+    UpdArgs ua{};
+    ua.n = n;
+    ua.ld = ld;
+    ua.w = w;
+    ua.m = m;
+    ua.mp = mp;
+    ua.skip = status.p + 5;
+    ua.part = colpart.p;
+    {
+      ProfScope ps(ctx, PROF_UPDATE, 2.0 * n * ld * sizeof(T) + 5.0 * n * mp * sizeof(T));
+      k_update_resid<T, 2><<<grid_fast, kFThreads, upd_smem, ctx->stream>>>(
+          S.p, AS.p, bw.p, sp.jacobi ? prec.p : nullptr, M.p, theta.p, ua);
+      MG_CHECK_LAUNCH(ctx);
+    }
+    k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, grid_fast, 2 * mp, colred.p);
+    MG_CHECK_LAUNCH(ctx);
+    MG_CUDA(cudaMemcpyAsync(colred.p + 2 * mp, theta.p, mp * sizeof(double),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+    MG_CUDA(cudaMemcpyAsync(colred.p + 3 * mp, status.p, 6 * sizeof(int), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    std::vector<double> buf(3 * mp + 3);
+    d2h_sync(ctx, buf.data(), colred.p, buf.size() * sizeof(double));
+    int st6[6];
+    std::memcpy(st6, buf.data() + 3 * mp, 6 * sizeof(int));
+    if (st6[4] != 0) {
+      std::vector<double> gb((size_t)w * w), ga((size_t)w * w);
+      d2h_sync(ctx, gb.data(), Gr0.p, gb.size() * sizeof(double));
+      d2h_sync(ctx, ga.data(), Gr1.p, ga.size() * sizeof(double));
+      int nb_bad = 0, na_bad = 0, first = -1;
+      double dmin = 1e300, dmax = 0;
+      for (size_t e = 0; e < gb.size(); ++e) {
+        if (!std::isfinite(gb[e])) { ++nb_bad; if (first < 0) first = (int)e; }
+        if (!std::isfinite(ga[e])) ++na_bad;
+      }
+      for (int c = 0; c < w; ++c) {
+        dmin = std::min(dmin, gb[(size_t)c * w + c]);
+        dmax = std::max(dmax, gb[(size_t)c * w + c]);
+      }
+      std::string cols;
+      for (int v : vcols) cols += std::to_string(v) + ",";
+      throw Error(MG_ERR_INTERNAL,
+                  "non-finite values in the fast-path Gram matrices (stage mask " +
+                      std::to_string(st6[4]) + ") iter " + std::to_string(iter_now) + " m " +
+                      std::to_string(m) + " GB bad " + std::to_string(nb_bad) + " first " +
+                      std::to_string(first) + " GA bad " + std::to_string(na_bad) +
+                      " diag range " + std::to_string(dmin) + " " + std::to_string(dmax) +
+                      " vcols " + cols);
+    }
+    ++fast_steps;
+    if (st6[5]) {
+      ++fast_fallbacks;
+      return false;
+    }
+    cr.assign(buf.begin(), buf.begin() + 2 * mp);
+    th.assign(buf.begin() + 2 * mp, buf.begin() + 3 * mp);
+    std::memcpy(st, st6, 4 * sizeof(int));
+    debug_check("fast-update");
+    return true;
+  }
+
   SolveResult run(double anorm_in, const double *b_dev, const double *diag_dev, double *eigvecs) {
     SolveResult res;
     require(m >= 1, MG_ERR_INPUT, "block size must be >= 1, got " + std::to_string(m));
@@ -1094,16 +1241,12 @@ struct Lobpcg {
     std::vector<double> rn;
     std::vector<int> cv;
     int st[4] = {m, m, m, m};
+    fast_setup();
+    iterate_sync(true, cr, th, st);  // residual block of the initial Ritz vectors
     int it = 0;
     for (it = 1; it <= sp.max_iter; ++it) {
       iter_now = it;
-      iterate_sync(true, cr, th, st);
       debug_check("resid");
-      if (it > 1 && st[1] < m) {  // basis collapsed last iteration (eigensolver.py:260-266)
-        orth_refill_rr(st[1]);
-        pcount = 0;
-        iterate_sync(true, cr, th, st);
-      }
       bool all = conv_test(rn, cv);
       double ts = 0.0;
       for (int c = 0; c < m; ++c) ts += th[c];
@@ -1119,7 +1262,7 @@ struct Lobpcg {
         if (!cv[c]) vcols.push_back(2 * mp + c);
       deflate_cols(2 * mp, 3 * mp, 2 * mp, mp);
       const bool prefix = (it % 32) != 0;
-      if (sizeof(T) == 4 && !prefix) {
+      if (sizeof(T) == 4 && (it % refresh_period()) == 0) {
         // fp32: carried A-images drift at fp32 resolution; refresh [AX AP AW]
         // with one wide SpMM at every full re-orthonormalisation
         spmm_cols(0, 3 * mp);
@@ -1127,55 +1270,59 @@ struct Lobpcg {
         spmm_cols(2 * mp, mp);
       }
       for (int c = 0; c < pcount; ++c) vcols.push_back(mp + c);
-      if (prefix) {
-        for (int rep = 0; rep < 2; ++rep) {
-          if (rep == 0) {
-            GramSpec gp = gspec(0, mp, mp, 2 * mp, 0, 0);
-            pass(0, 0, 0, 0, 0, 0, 0, &gp, 1, Gr0.p, nullptr);
+      bool done = false;
+      if (prefix && fast_ok) done = fast_iteration(vcols, cr, th, st);
+      if (!done) {
+        if (prefix) {
+          for (int rep = 0; rep < 2; ++rep) {
+            if (rep == 0) {
+              GramSpec gp = gspec(0, mp, mp, 2 * mp, 0, 0);
+              pass(0, 0, 0, 0, 0, 0, 0, &gp, 1, Gr0.p, nullptr);
+            }
+            ProjArgs pa{};
+            pa.nx = m;
+            pa.rows = mp;
+            pa.g_c0 = mp;
+            pa.g_cw = 2 * mp;
+            pa.o0 = mp;
+            pa.ow = 2 * mp;
+            pa.nv = (int)vcols.size();
+            for (int i = 0; i < pa.nv; ++i) pa.vcols[i] = vcols[i];
+            pa.denom = 1.0;
+            k_ctrl_proj<T><<<1, 256, 0, ctx->stream>>>(pa, Gr0.p, M.p);
+            MG_CHECK_LAUNCH(ctx);
+            GramSpec gn = rep == 0 ? gspec(0, mp, mp, 2 * mp, 0, 0)
+                                   : gspec(mp, 2 * mp, mp, 2 * mp, 1, 0);
+            pass(1, 1, 1, 0, mp, mp, 2 * mp, &gn, 1, Gr0.p, nullptr);
           }
-          ProjArgs pa{};
-          pa.nx = m;
-          pa.rows = mp;
-          pa.g_c0 = mp;
-          pa.g_cw = 2 * mp;
-          pa.o0 = mp;
-          pa.ow = 2 * mp;
-          pa.nv = (int)vcols.size();
-          for (int i = 0; i < pa.nv; ++i) pa.vcols[i] = vcols[i];
-          pa.denom = 1.0;
-          k_ctrl_proj<T><<<1, 256, 0, ctx->stream>>>(pa, Gr0.p, M.p);
-          MG_CHECK_LAUNCH(ctx);
-          GramSpec gn = rep == 0 ? gspec(0, mp, mp, 2 * mp, 0, 0)
-                                 : gspec(mp, 2 * mp, mp, 2 * mp, 1, 0);
-          pass(1, 1, 1, 0, mp, mp, 2 * mp, &gn, 1, Gr0.p, nullptr);
+          ortho(vcols, mp, 2 * mp, 1.0, mp, 2 * mp, mp, 2 * mp);
+          GramSpec g2[2] = {gspec(mp, 2 * mp, mp, 2 * mp, 1, 0),
+                            gspec(0, 3 * mp, 0, 3 * mp, 1, 1)};
+          pass(1, 0, 1, mp, 2 * mp, mp, 2 * mp, g2, 2, Gr0.p, Gr1.p);
+          rr(m, mp, 2 * mp, 3 * mp, true);
+        } else {
+          std::vector<int> order;
+          for (int c = 0; c < m; ++c) order.push_back(c);
+          for (int v : vcols) order.push_back(v);
+          GramSpec gf = gspec(0, 3 * mp, 0, 3 * mp, 1, 0);
+          pass(0, 0, 0, 0, 0, 0, 0, &gf, 1, Gr0.p, nullptr);
+          ortho(order, 0, 3 * mp, 0.0, 0, 3 * mp, 0, 3 * mp);
+          GramSpec g2[2] = {gspec(0, 3 * mp, 0, 3 * mp, 1, 0),
+                            gspec(0, 3 * mp, 0, 3 * mp, 1, 1)};
+          pass(1, 0, 1, 0, 3 * mp, 0, 3 * mp, g2, 2, Gr0.p, Gr1.p);
+          rr(0, 0, 3 * mp, 3 * mp, true);
         }
-        ortho(vcols, mp, 2 * mp, 1.0, mp, 2 * mp, mp, 2 * mp);
-        GramSpec g2[2] = {gspec(mp, 2 * mp, mp, 2 * mp, 1, 0),
-                          gspec(0, 3 * mp, 0, 3 * mp, 1, 1)};
-        pass(1, 0, 1, mp, 2 * mp, mp, 2 * mp, g2, 2, Gr0.p, Gr1.p);
-        rr(m, mp, 2 * mp, 3 * mp, true);
-      } else {
-        std::vector<int> order;
-        for (int c = 0; c < m; ++c) order.push_back(c);
-        for (int v : vcols) order.push_back(v);
-        GramSpec gf = gspec(0, 3 * mp, 0, 3 * mp, 1, 0);
-        pass(0, 0, 0, 0, 0, 0, 0, &gf, 1, Gr0.p, nullptr);
-        ortho(order, 0, 3 * mp, 0.0, 0, 3 * mp, 0, 3 * mp);
-        GramSpec g2[2] = {gspec(0, 3 * mp, 0, 3 * mp, 1, 0), gspec(0, 3 * mp, 0, 3 * mp, 1, 1)};
-        pass(1, 0, 1, 0, 3 * mp, 0, 3 * mp, g2, 2, Gr0.p, Gr1.p);
-        rr(0, 0, 3 * mp, 3 * mp, true);
+        pass(1, 0, 1, 0, 3 * mp, 0, 2 * mp, nullptr, 0, nullptr, nullptr);
+        iterate_sync(true, cr, th, st);
       }
-      pass(1, 0, 1, 0, 3 * mp, 0, 2 * mp, nullptr, 0, nullptr, nullptr);
-      pcount = m;  // corrected at the next sync if the basis collapsed
-    }
-    if (it > sp.max_iter) {
-      it = sp.max_iter;
-      if (it >= 1) {
-        int s2[4];
-        d2h_sync(ctx, s2, status.p, sizeof(s2));
-        if (s2[1] < m) orth_refill_rr(s2[1]);
+      pcount = m;
+      if (st[1] < m) {  // basis collapsed (eigensolver.py:260-266)
+        orth_refill_rr(st[1]);
+        pcount = 0;
+        iterate_sync(true, cr, th, st);
       }
     }
+    if (it > sp.max_iter) it = sp.max_iter;
     res.iterations = it;
     // ---- honest final report (eigensolver.py:268-283)
     fresh_theta(th);
@@ -1234,6 +1381,8 @@ struct Lobpcg {
     MG_CHECK_LAUNCH(ctx);
     sync(ctx);
     res.normals_used = zpos;
+    res.fast_steps = fast_steps;
+    res.fast_fallbacks = fast_fallbacks;
     return res;
   }
 };
