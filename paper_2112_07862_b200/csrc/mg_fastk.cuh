@@ -9,6 +9,7 @@
 #pragma once
 #include "mg_block.cuh"
 #include "mg_small.cuh"
+#include "mg_eig.cuh"
 
 namespace mg {
 
@@ -51,12 +52,13 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// issue the copies of row tile `tile` (rows [tile*TK, ...)) into ring stage st
+// issue the copies of row tile `tile` (rows [tile*tk, ...)) into ring stage st
 template <typename T>
 __device__ __forceinline__ void issue_tile(const T *S, const T *AS, const T *b, int64_t n, int ld,
-                                           int64_t tile, T *sS, T *sA, T *sb, uint64_t *bar) {
-  int64_t r0 = tile * kFTK;
-  int nr = (int)min((int64_t)kFTK, n - r0);
+                                           int tk, int64_t tile, T *sS, T *sA, T *sb,
+                                           uint64_t *bar) {
+  int64_t r0 = tile * tk;
+  int nr = (int)min((int64_t)tk, n - r0);
   uint32_t bytes_m = (uint32_t)(nr * ld * sizeof(T));
   uint32_t bytes_b = (uint32_t)(((nr * sizeof(T)) + 15) / 16 * 16);
   uint32_t total = bytes_m * (AS ? 2 : 1) + (b ? bytes_b : 0);
@@ -73,6 +75,7 @@ __device__ __forceinline__ void issue_tile(const T *S, const T *AS, const T *b, 
 // fp64 data accumulates in fp64 registers.
 struct Gram2Args {
   int64_t n;
+  int tk;                 // rows per tile
   int ld, w, nb;          // w columns [0, w), nb = ceil(w/8) blocks per side
   int blk_lo, nbr;        // Gram blocks [blk_lo, blk_lo + nbr) of the enumeration
   int nsym;               // blocks per Gram: nb*(nb+1)/2
@@ -97,14 +100,14 @@ __global__ void __launch_bounds__(kFThreads, 1)
             Gram2Args a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   constexpr bool F32 = sizeof(T) == 4;
-  const int ld = a.ld;
-  const size_t tile_elems = (size_t)kFTK * ld + 16;
+  const int ld = a.ld, TK = a.tk;
+  const size_t tile_elems = (size_t)TK * ld + 16;
   T *ring = reinterpret_cast<T *>(smraw);
   // stage s: S tile, AS tile, b tile
-  auto stS = [&](int s) { return ring + (size_t)s * (2 * tile_elems + kFTK + 16); };
+  auto stS = [&](int s) { return ring + (size_t)s * (2 * tile_elems + TK + 16); };
   auto stA = [&](int s) { return stS(s) + tile_elems; };
   auto stB = [&](int s) { return stS(s) + 2 * tile_elems; };
-  unsigned char *after = smraw + (size_t)NS * (2 * tile_elems + kFTK + 16) * sizeof(T);
+  unsigned char *after = smraw + (size_t)NS * (2 * tile_elems + TK + 16) * sizeof(T);
   after = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(after) + 15) & ~uintptr_t(15));
   uint64_t *bars = reinterpret_cast<uint64_t *>(after);
   double *acc64 = reinterpret_cast<double *>(after + 64);  // [64][kFThreads]
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
   int g = 0, bi = 0, bj = 0;
   if (active) gram2_decode(a.blk_lo + blk, a.nb, a.nsym, g, bi, bj);
 
-  const int64_t ntiles = (a.n + kFTK - 1) / kFTK;
+  const int64_t ntiles = (a.n + TK - 1) / TK;
   const int64_t t_begin = ntiles * blockIdx.x / gridDim.x;
   const int64_t t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
 
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
   __syncthreads();
   if (tid == 0)
     for (int s = 0; s < NS && t_begin + s < t_end; ++s)
-      issue_tile(S, AS, b, a.n, ld, t_begin + s, stS(s), stA(s), stB(s), &bars[s]);
+      issue_tile(S, AS, b, a.n, ld, TK, t_begin + s, stS(s), stA(s), stB(s), &bars[s]);
 
   float accf[64];
   double accd[F32 ? 1 : 64];
@@ -144,17 +147,30 @@ __global__ void __launch_bounds__(kFThreads, 1)
     const int s = (int)((t - t_begin) % NS);
     const uint32_t phase = (uint32_t)(((t - t_begin) / NS) & 1);
     mbar_wait(&bars[s], phase);
-    const int nr = (int)min((int64_t)kFTK, a.n - t * kFTK);
+    const int nr = (int)min((int64_t)TK, a.n - t * TK);
     if (active) {
       const T *U = stS(s) + bi * 8;
       const T *Vb = (g == 0 ? stS(s) : stA(s)) + bj * 8;
       const T *bb = stB(s);
       for (int r = grp; r < nr; r += G) {
         T u[8], v[8];
+        if constexpr (F32) {
+          const float4 u0 = reinterpret_cast<const float4 *>(U + r * ld)[0];
+          const float4 u1 = reinterpret_cast<const float4 *>(U + r * ld)[1];
+          const float4 v0 = reinterpret_cast<const float4 *>(Vb + r * ld)[0];
+          const float4 v1 = reinterpret_cast<const float4 *>(Vb + r * ld)[1];
+          u[0] = u0.x; u[1] = u0.y; u[2] = u0.z; u[3] = u0.w;
+          u[4] = u1.x; u[5] = u1.y; u[6] = u1.z; u[7] = u1.w;
+          v[0] = v0.x; v[1] = v0.y; v[2] = v0.z; v[3] = v0.w;
+          v[4] = v1.x; v[5] = v1.y; v[6] = v1.z; v[7] = v1.w;
+        } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          u[q] = U[r * ld + q];
-          v[q] = Vb[r * ld + q];
+          for (int q = 0; q < 8; q += 2) {
+            const double2 uu = *reinterpret_cast<const double2 *>(U + r * ld + q);
+            const double2 vv = *reinterpret_cast<const double2 *>(Vb + r * ld + q);
+            u[q] = uu.x; u[q + 1] = uu.y;
+            v[q] = vv.x; v[q + 1] = vv.y;
+          }
         }
         if (g == 0) {
           const T wr = bb[r];
@@ -179,9 +195,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
     __syncthreads();  // everyone is done with stage s
     if (tid == 0 && t + NS < t_end) {
       fence_proxy_async();
-      issue_tile(S, AS, b, a.n, ld, t + NS, stS(s), stA(s), stB(s), &bars[s]);
+      issue_tile(S, AS, b, a.n, ld, TK, t + NS, stS(s), stA(s), stB(s), &bars[s]);
     }
-    if (F32 && ++since_flush == 1) {
+    since_flush += (nr + G - 1) / G;  // rows this thread accumulated in fp32
+    if (F32 && since_flush >= 32) {
       since_flush = 0;
       if (active) {
 #pragma unroll
@@ -244,41 +261,43 @@ __global__ void k_reduce_gram2(const double *__restrict__ part, int nb_cta, int 
 // M layout (T, row-major): Zp [w x mp] then Yx [mp x mp].
 struct UpdArgs {
   int64_t n;
+  int tk;
   int ld, w, m, mp;
   const int *skip;        // device flag: nonzero -> return (fallback iteration)
   double *part;           // [grid][2*mp]
+  void *wc;               // compact W copy (n x mp), the SpMM input
 };
 
-template <typename T, int NS>
+template <typename T, int NS, int RT>
 __global__ void __launch_bounds__(kFThreads, 1)
     k_update_resid(T *__restrict__ S, T *__restrict__ AS, const T *__restrict__ b,
                    const T *__restrict__ prec, const T *__restrict__ Mg,
                    const double *__restrict__ theta, UpdArgs a) {
   if (*a.skip) return;
   extern __shared__ __align__(128) unsigned char smraw[];
-  const int ld = a.ld, w = a.w, mp = a.mp;
-  const size_t tile_elems = (size_t)kFTK * ld + 16;
+  const int ld = a.ld, w = a.w, mp = a.mp, TK = a.tk;
+  const size_t tile_elems = (size_t)TK * ld + 16;
   T *ring = reinterpret_cast<T *>(smraw);
-  auto stS = [&](int s) { return ring + (size_t)s * (2 * tile_elems + kFTK + 16); };
+  auto stS = [&](int s) { return ring + (size_t)s * (2 * tile_elems + TK + 16); };
   auto stA = [&](int s) { return stS(s) + tile_elems; };
   auto stB = [&](int s) { return stS(s) + 2 * tile_elems; };
-  T *sM = ring + (size_t)NS * (2 * tile_elems + kFTK + 16);   // Zp then Yx
+  T *sM = ring + (size_t)NS * (2 * tile_elems + TK + 16);   // Zp then Yx
   const int mlen = w * mp + mp * mp;
-  T *oPS = sM + mlen + 16;                                     // [TK][mp] each
-  T *oPA = oPS + kFTK * mp;
-  T *oXS = oPA + kFTK * mp;
-  T *oXA = oXS + kFTK * mp;
-  T *sth = oXA + kFTK * mp;                                    // theta (mp)
-  T *sprec = sth + mp + 4;                                     // prec tile (TK)
-  unsigned char *after = reinterpret_cast<unsigned char *>(sprec + kFTK + 4);
+  T *oPS = sM + mlen + 16;                                   // [TK][mp] each
+  T *oPA = oPS + TK * mp;
+  T *oXS = oPA + TK * mp;
+  T *oXA = oXS + TK * mp;
+  T *sth = oXA + TK * mp;                                    // theta (mp)
+  T *sprec = sth + mp + 4;                                   // prec tile (TK)
+  unsigned char *after = reinterpret_cast<unsigned char *>(sprec + TK + 4);
   after = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(after) + 15) & ~uintptr_t(15));
   uint64_t *bars = reinterpret_cast<uint64_t *>(after);
-  double *red = reinterpret_cast<double *>(after + 64);       // [kFThreads][2]
+  double *red = reinterpret_cast<double *>(after + 64);     // [kFThreads][2]
 
   const int tid = threadIdx.x;
   for (int e = tid; e < mlen; e += kFThreads) sM[e] = Mg[e];
   for (int e = tid; e < mp; e += kFThreads) sth[e] = e < a.m ? (T)theta[e] : T(0);
-  const int64_t ntiles = (a.n + kFTK - 1) / kFTK;
+  const int64_t ntiles = (a.n + TK - 1) / TK;
   const int64_t t_begin = ntiles * blockIdx.x / gridDim.x;
   const int64_t t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
   if (tid == 0) {
@@ -288,81 +307,83 @@ __global__ void __launch_bounds__(kFThreads, 1)
   __syncthreads();
   if (tid == 0)
     for (int s = 0; s < NS && t_begin + s < t_end; ++s)
-      issue_tile<T>(S, AS, b, a.n, ld, t_begin + s, stS(s), stA(s), stB(s), &bars[s]);
+      issue_tile<T>(S, AS, b, a.n, ld, TK, t_begin + s, stS(s), stA(s), stB(s), &bars[s]);
 
-  // residual norm accumulators: thread owns column (tid % mp) for rows tid/mp + k*R
   const int R = kFThreads / mp;
   const int rc = tid % mp, rrow = tid / mp;
   double sr = 0.0, sx = 0.0;
   const T *Zp = sM, *Yx = sM + w * mp;
-  // output tiles: (8 rows x 4 cols) register blocks over [TK x mp] per matrix
-  const int cb = (mp + 3) / 4, nblk = (kFTK / 8) * cb;  // per matrix
+  const int cb = (mp + 3) / 4, nblk = (TK / RT) * cb;  // per matrix
   for (int64_t t = t_begin; t < t_end; ++t) {
     const int s = (int)((t - t_begin) % NS);
     const uint32_t phase = (uint32_t)(((t - t_begin) / NS) & 1);
     mbar_wait(&bars[s], phase);
-    const int64_t r0 = t * kFTK;
-    const int nr = (int)min((int64_t)kFTK, a.n - r0);
-    for (int e = tid; e < kFTK; e += kFThreads) sprec[e] = (e < nr && prec) ? prec[r0 + e] : T(1);
-    // P_new for S and AS
-    for (int job = tid; job < 2 * nblk; job += kFThreads) {
-      const int mat = job / nblk, jb = job - mat * nblk;
-      const int rb = jb / cb, c0 = (jb - rb * cb) * 4;
-      const T *src = (mat ? stA(s) : stS(s)) + rb * 8 * ld;
-      T acc[8][4];
+    const int64_t r0 = t * TK;
+    const int nr = (int)min((int64_t)TK, a.n - r0);
+    for (int e = tid; e < TK; e += kFThreads) sprec[e] = (e < nr && prec) ? prec[r0 + e] : T(1);
+    // P_new = S Zp, then X_new = X Yx + P_new  (register blocks of RT rows x 4
+    // columns; fp32 reads 4 consecutive k of each row with one 128-bit load)
+    for (int phase = 0; phase < 2; ++phase) {
+      const int K = phase == 0 ? w : mp;
+      const T *Bm = phase == 0 ? Zp : Yx;
+      for (int job = tid; job < 2 * nblk; job += kFThreads) {
+        const int mat = job / nblk, jb = job - mat * nblk;
+        const int rb = jb / cb, c0 = (jb - rb * cb) * 4;
+        const T *src = (mat ? stA(s) : stS(s)) + rb * RT * ld;
+        T acc[RT][4];
+        if (phase == 0) {
 #pragma unroll
-      for (int x = 0; x < 8; ++x)
+          for (int x = 0; x < RT; ++x)
 #pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = T(0);
-      for (int k = 0; k < w; ++k) {
-        T mz[4];
+            for (int y = 0; y < 4; ++y) acc[x][y] = T(0);
+        } else {
+          const T *pn = (mat ? oPA : oPS) + rb * RT * mp + c0;
 #pragma unroll
-        for (int y = 0; y < 4; ++y) mz[y] = Zp[k * mp + c0 + y];
+          for (int x = 0; x < RT; ++x)
 #pragma unroll
-        for (int x = 0; x < 8; ++x) {
-          const T u = src[x * ld + k];
-#pragma unroll
-          for (int y = 0; y < 4; ++y) acc[x][y] += u * mz[y];
+            for (int y = 0; y < 4; ++y) acc[x][y] = (c0 + y < mp) ? pn[x * mp + y] : T(0);
         }
-      }
-      T *dst = (mat ? oPA : oPS) + rb * 8 * mp + c0;
+        if constexpr (sizeof(T) == 4) {
+          for (int k = 0; k < K; k += 4) {
+            float4 b[4];
 #pragma unroll
-      for (int x = 0; x < 8; ++x)
+            for (int kk = 0; kk < 4; ++kk)
+              b[kk] = *reinterpret_cast<const float4 *>(Bm + (k + kk) * mp + c0);
 #pragma unroll
-        for (int y = 0; y < 4; ++y)
-          if (c0 + y < mp) dst[x * mp + y] = acc[x][y];
-    }
-    __syncthreads();
-    // X_new = X Yx + P_new
-    for (int job = tid; job < 2 * nblk; job += kFThreads) {
-      const int mat = job / nblk, jb = job - mat * nblk;
-      const int rb = jb / cb, c0 = (jb - rb * cb) * 4;
-      const T *src = (mat ? stA(s) : stS(s)) + rb * 8 * ld;
-      const T *pn = (mat ? oPA : oPS) + rb * 8 * mp + c0;
-      T acc[8][4];
+            for (int x = 0; x < RT; ++x) {
+              const float4 av = *reinterpret_cast<const float4 *>(src + x * ld + k);
+              const float aa[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
-      for (int x = 0; x < 8; ++x)
+              for (int kk = 0; kk < 4; ++kk) {
+                acc[x][0] += aa[kk] * b[kk].x;
+                acc[x][1] += aa[kk] * b[kk].y;
+                acc[x][2] += aa[kk] * b[kk].z;
+                acc[x][3] += aa[kk] * b[kk].w;
+              }
+            }
+          }
+        } else {
+          for (int k = 0; k < K; ++k) {
+            T mz[4];
 #pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = (c0 + y < mp) ? pn[x * mp + y] : T(0);
-      for (int k = 0; k < mp; ++k) {
-        T my[4];
+            for (int y = 0; y < 4; ++y) mz[y] = Bm[k * mp + c0 + y];
 #pragma unroll
-        for (int y = 0; y < 4; ++y) my[y] = Yx[k * mp + c0 + y];
+            for (int x = 0; x < RT; ++x) {
+              const T u = src[x * ld + k];
 #pragma unroll
-        for (int x = 0; x < 8; ++x) {
-          const T u = src[x * ld + k];
-#pragma unroll
-          for (int y = 0; y < 4; ++y) acc[x][y] += u * my[y];
+              for (int y = 0; y < 4; ++y) acc[x][y] += u * mz[y];
+            }
+          }
         }
+        T *dst = (phase == 0 ? (mat ? oPA : oPS) : (mat ? oXA : oXS)) + rb * RT * mp + c0;
+#pragma unroll
+        for (int x = 0; x < RT; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y)
+            if (c0 + y < mp) dst[x * mp + y] = acc[x][y];
       }
-      T *dst = (mat ? oXA : oXS) + rb * 8 * mp + c0;
-#pragma unroll
-      for (int x = 0; x < 8; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y)
-          if (c0 + y < mp) dst[x * mp + y] = acc[x][y];
+      __syncthreads();
     }
-    __syncthreads();
     // residual + W, and write back [X P W] / [AX AP] rows
     for (int rr = rrow; rr < nr && rrow < R; rr += R) {
       const T x = oXS[rr * mp + rc];
@@ -380,13 +401,14 @@ __global__ void __launch_bounds__(kFThreads, 1)
       srow[rc] = x;
       srow[mp + rc] = oPS[rr * mp + rc];
       srow[2 * mp + rc] = wv;
+      reinterpret_cast<T *>(a.wc)[(r0 + rr) * mp + rc] = wv;
       arow[rc] = ax;
       arow[mp + rc] = oPA[rr * mp + rc];
     }
     __syncthreads();  // stage s and the output tiles are free
     if (tid == 0 && t + NS < t_end) {
       fence_proxy_async();
-      issue_tile<T>(S, AS, b, a.n, ld, t + NS, stS(s), stA(s), stB(s), &bars[s]);
+      issue_tile<T>(S, AS, b, a.n, ld, TK, t + NS, stS(s), stA(s), stB(s), &bars[s]);
     }
   }
   red[tid * 2] = (rrow < R) ? sr : 0.0;
@@ -418,6 +440,7 @@ struct FastArgs {
   double fast_tol;
   double rel_tol, abs_tol;
   int use_global;
+  int clk_off;            // >0: write phase clocks at scratch[clk_off...] (debug)
 };
 
 template <typename T>
@@ -427,16 +450,23 @@ __global__ void __launch_bounds__(512)
   extern __shared__ __align__(16) double smf[];
   __shared__ int keep[kMaxFast];
   __shared__ int rank[kMaxFast];
-  __shared__ int perm[kMaxFast];
-  __shared__ int pidx[kMaxFast + 2];
-  __shared__ double cs[kMaxFast + 2];
   __shared__ double wv[kMaxFast];
   __shared__ double orig[kMaxFast];
   __shared__ double unproj[kMaxFast];
   __shared__ double red[512];
-  __shared__ int cnt, bad;
+  __shared__ double red2[512];
+  __shared__ double et[kMaxFast], ed[kMaxFast], ee[kMaxFast], elo[kMaxFast], ehi[kMaxFast];
+  __shared__ int ecnt[512];
+  __shared__ int bad;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int m = a.m, nv = a.nv, w = a.w, mp = a.mp;
+  long long *tclk = reinterpret_cast<long long *>(scratch + a.clk_off);
+  int tph = 0;
+#define MG_TICK() \
+  do {              \
+    if (a.clk_off > 0 && tid == 0) tclk[tph++] = clock64(); \
+  } while (0)
+  MG_TICK();
   // global scratch: C, D [m x nv]; RX, RXi [m x m]; T, HT [w x smax]
   double *C = scratch;
   double *D = C + m * nv;
@@ -460,6 +490,7 @@ __global__ void __launch_bounds__(512)
     return;
   }
   blk_tri_inv_kept(RX, m, m, keep, RXi, m);
+  MG_TICK();
   for (int e = tid; e < m * nv; e += nt) {  // C = RX^-T G_XV
     int x = e / nv, q = e - x * nv;
     double s2 = 0.0;
@@ -481,6 +512,7 @@ __global__ void __launch_bounds__(512)
     if (p == q) unproj[p] = GB[a.vcols[p] * w + a.vcols[p]];
   }
   __syncthreads();
+  MG_TICK();
   blk_check_finite(Gv, nv, nv, nv, status + 4, 16);
   const int nk = blk_cholesky_drop(Gv, nv, nv, 1.0, R, nv, keep, orig, a.rel_tol, a.abs_tol);
   // quality: every kept pivot must be resolvable from the Gram at this precision
@@ -494,7 +526,9 @@ __global__ void __launch_bounds__(512)
     if (tid == 0) status[5] = 1;
     return;
   }
+  MG_TICK();
   blk_tri_inv_kept(R, nv, nv, keep, Gv, nv);  // Gv <- Rinv
+  MG_TICK();
   if (tid == 0) {
     int r = 0;
     for (int t = 0; t < nv; ++t) rank[t] = keep[t] ? r++ : -1;
@@ -517,6 +551,7 @@ __global__ void __launch_bounds__(512)
     Tm[x * s + m + rank[t]] = -s2;
   }
   __syncthreads();
+  MG_TICK();
   for (int e = tid; e < w * s; e += nt) {  // HT = G_A T
     int i = e / s, j = e - i * s;
     double s2 = 0.0;
@@ -548,29 +583,34 @@ __global__ void __launch_bounds__(512)
     }
   }
   __syncthreads();
+  MG_TICK();
   blk_check_finite(Aj, s, s, s, status + 4, 8);
-  blk_jacobi(Aj, s, s, Vj, s, wv, cs, pidx, perm, &cnt, red);
   const int take = min(m, s);
+  {
+    double *lu = big + 2 * nv * nv + 2 * (size_t)smax * smax;  // dedicated LU scratch
+    EigWork ew{et, ed, ee, elo, ehi, ecnt, red, red2, lu};
+    if (a.clk_off > 0) ew.clk = tclk + 20;
+    blk_eig_smallest(Aj, s, s, take, wv, Vj, take, ew);
+  }
+  MG_TICK();
   for (int i = tid; i < take; i += nt) theta[i] = wv[i];
-  // Zp [w x mp] = T[:, m:s] Y[m:s, :take];  Yx [mp x mp] = Y[0:m, :take]
+  // Zp [w x mp] = T[:, m:s] Y[m:s, :take];  Yx [mp x mp] = RX^-1 Y[0:m, :take]
   for (int e = tid; e < w * mp; e += nt) {
     int r = e / mp, c = e - r * mp;
     double s2 = 0.0;
-    if (c < take) {
-      int col = perm[c];
-      for (int u = m; u < s; ++u) s2 += Tm[r * s + u] * Vj[u * s + col];
-    }
+    if (c < take)
+      for (int u = m; u < s; ++u) s2 += Tm[r * s + u] * Vj[u * take + c];
     Mout[e] = (T)s2;
   }
-  for (int e = tid; e < mp * mp; e += nt) {  // Yx = RX^-1 Y[0:m, :take]
+  for (int e = tid; e < mp * mp; e += nt) {
     int x = e / mp, c = e - x * mp;
     double v = 0.0;
-    if (x < m && c < take) {
-      int col = perm[c];
-      for (int y = x; y < m; ++y) v += RXi[x * m + y] * Vj[y * s + col];
-    }
+    if (x < m && c < take)
+      for (int y = x; y < m; ++y) v += RXi[x * m + y] * Vj[y * take + c];
     Mout[w * mp + e] = (T)v;
   }
+  __syncthreads();
+  MG_TICK();
   if (tid == 0) {
     status[0] = nk;
     status[1] = take;
@@ -578,6 +618,7 @@ __global__ void __launch_bounds__(512)
     status[3] = s;
     status[5] = 0;
   }
+#undef MG_TICK
 }
 
 }  // namespace mg

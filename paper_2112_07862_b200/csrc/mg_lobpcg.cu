@@ -27,6 +27,7 @@
 #include "mg_graph.cuh"
 #include "mg_small.cuh"
 #include "mg_fastk.cuh"
+#include "mg_eig.cuh"
 
 namespace mg {
 
@@ -73,7 +74,55 @@ void make_solver_csr(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *
 // ------------------------------------------------------------------ SpMM ---
 // Sub-warp of L lanes per CSR row; lane l owns columns [l*VN, l*VN+VN) of the
 // row-major block, so each nonzero costs one 16-byte coalesced load of the
-// neighbour's row segment.  Four nonzeros in flight per lane.
+// neighbour's row segment.  Four nonzeros in flight per lane.  The matrix is
+// streamed once (L2 evict-first, no L1 allocation); the gathered block rows
+// are re-read ~nnz/row times and are kept in L2 (evict-last).
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int ld_stream_i32(const int *a, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_stream(const float *a, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
+               : "=f"(v)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_stream(const double *a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float4 ld_keep(const float4 *a, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ld_keep(const double2 *a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(a), "l"(pol));
+  return v;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256)
     k_spmm(int64_t n, const int64_t *__restrict__ ptr, const int *__restrict__ idx,
@@ -85,6 +134,7 @@ __global__ void __launch_bounds__(256)
   int G = 32 / L;
   int g = lane / L, gl = lane - g * L;
   if (g >= G) return;
+  const uint64_t pf = l2_policy_first(), pl = l2_policy_last();
   int64_t per_block = (int64_t)(blockDim.x >> 5) * G;
   int64_t stride = (int64_t)gridDim.x * per_block;
   for (int64_t row = blockIdx.x * per_block + (threadIdx.x >> 5) * G + g; row < n; row += stride) {
@@ -94,14 +144,14 @@ __global__ void __launch_bounds__(256)
     for (int q = 0; q < VN; ++q) acc[q] = T(0);
     int64_t k = s;
     for (; k + 4 <= e; k += 4) {
-      int j0 = __ldg(idx + k), j1 = __ldg(idx + k + 1), j2 = __ldg(idx + k + 2),
-          j3 = __ldg(idx + k + 3);
-      T v0 = __ldg(val + k), v1 = __ldg(val + k + 1), v2 = __ldg(val + k + 2),
-        v3 = __ldg(val + k + 3);
-      V x0 = __ldg(reinterpret_cast<const V *>(X + (int64_t)j0 * ldx) + gl);
-      V x1 = __ldg(reinterpret_cast<const V *>(X + (int64_t)j1 * ldx) + gl);
-      V x2 = __ldg(reinterpret_cast<const V *>(X + (int64_t)j2 * ldx) + gl);
-      V x3 = __ldg(reinterpret_cast<const V *>(X + (int64_t)j3 * ldx) + gl);
+      int j0 = ld_stream_i32(idx + k, pf), j1 = ld_stream_i32(idx + k + 1, pf),
+          j2 = ld_stream_i32(idx + k + 2, pf), j3 = ld_stream_i32(idx + k + 3, pf);
+      T v0 = ld_stream(val + k, pf), v1 = ld_stream(val + k + 1, pf), v2 = ld_stream(val + k + 2, pf),
+        v3 = ld_stream(val + k + 3, pf);
+      V x0 = ld_keep(reinterpret_cast<const V *>(X + (int64_t)j0 * ldx) + gl, pl);
+      V x1 = ld_keep(reinterpret_cast<const V *>(X + (int64_t)j1 * ldx) + gl, pl);
+      V x2 = ld_keep(reinterpret_cast<const V *>(X + (int64_t)j2 * ldx) + gl, pl);
+      V x3 = ld_keep(reinterpret_cast<const V *>(X + (int64_t)j3 * ldx) + gl, pl);
       const T *p0 = reinterpret_cast<const T *>(&x0), *p1 = reinterpret_cast<const T *>(&x1),
               *p2 = reinterpret_cast<const T *>(&x2), *p3 = reinterpret_cast<const T *>(&x3);
 #pragma unroll
@@ -113,9 +163,9 @@ __global__ void __launch_bounds__(256)
       }
     }
     for (; k < e; ++k) {
-      int j0 = __ldg(idx + k);
-      T v0 = __ldg(val + k);
-      V x0 = __ldg(reinterpret_cast<const V *>(X + (int64_t)j0 * ldx) + gl);
+      int j0 = ld_stream_i32(idx + k, pf);
+      T v0 = ld_stream(val + k, pf);
+      V x0 = ld_keep(reinterpret_cast<const V *>(X + (int64_t)j0 * ldx) + gl, pl);
       const T *p0 = reinterpret_cast<const T *>(&x0);
 #pragma unroll
       for (int q = 0; q < VN; ++q) acc[q] += v0 * p0[q];
@@ -151,7 +201,7 @@ template <typename T>
 __global__ void k_resid(int64_t n, const T *__restrict__ S, const T *__restrict__ AS, int ld,
                         int m, int mp, int wcol, const double *__restrict__ theta,
                         const T *__restrict__ b, const T *__restrict__ prec, T *__restrict__ Wd,
-                        double *__restrict__ part) {
+                        double *__restrict__ part, T *__restrict__ Wc) {
   extern __shared__ double sm_r[];
   int R = blockDim.x / mp;
   int c = threadIdx.x % mp, rr = threadIdx.x / mp;
@@ -169,7 +219,10 @@ __global__ void k_resid(int64_t n, const T *__restrict__ S, const T *__restrict_
         sx += (double)x * (double)x;
         w = prec ? prec[row] * r : r;
       }
-      if (Wd) Wd[row * ld + wcol + c] = w;
+      if (Wd) {
+        Wd[row * ld + wcol + c] = w;
+        Wc[row * mp + c] = w;
+      }
     }
     sm_r[rr * 2 * mp + c] = sr;
     sm_r[rr * 2 * mp + mp + c] = sx;
@@ -625,13 +678,12 @@ __global__ void __launch_bounds__(kCtrlThreads)
   extern __shared__ __align__(16) double smr[];
   __shared__ int keep[kMaxL];
   __shared__ int rank[kMaxL];
-  __shared__ int perm[kMaxL];
-  __shared__ int pidx[kMaxL + 2];
-  __shared__ double cs[kMaxL + 2];
   __shared__ double w[kMaxL];
   __shared__ double red[kCtrlThreads];
-  __shared__ int cnt;
+  __shared__ double red2[kCtrlThreads];
   __shared__ double orig[kMaxL];
+  __shared__ double et[kMaxL], ed[kMaxL], ee[kMaxL], elo[kMaxL], ehi[kMaxL];
+  __shared__ int ecnt[kCtrlThreads];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int nk = status[0];
   // scratch layout (global): F [hw x smax], HF [hw x smax], (+ big matrices if use_global)
@@ -699,8 +751,12 @@ __global__ void __launch_bounds__(kCtrlThreads)
   }
   __syncthreads();
   blk_check_finite(Aj, s, s, s, status + 4, 8);
-  blk_jacobi(Aj, s, s, Vj, s, w, cs, pidx, perm, &cnt, red);
   const int take = min(a.m, s);
+  {
+    double *lu = big + 2 * nk * nk + 2 * (size_t)smax * smax;  // dedicated LU scratch
+    EigWork ew{et, ed, ee, elo, ehi, ecnt, red, red2, lu};
+    blk_eig_smallest(Aj, s, s, take, w, Vj, take, ew);
+  }
   for (int i = tid; i < take; i += nt) theta[i] = w[i];
   // 4. M5 = [F Y | F[:, m:] Y[m:]]   (rows physical [0, hw), cols [0, 2mp))
   const int ow = 2 * a.mp;
@@ -708,11 +764,10 @@ __global__ void __launch_bounds__(kCtrlThreads)
     int r = e / ow, c = e - r * ow;
     double acc = 0.0;
     if (c < take) {
-      int col = perm[c];
-      for (int u = 0; u < s; ++u) acc += F[r * s + u] * Vj[u * s + col];
+      for (int u = 0; u < s; ++u) acc += F[r * s + u] * Vj[u * take + c];
     } else if (a.want_p && c >= a.mp && c - a.mp < take) {
-      int col = perm[c - a.mp];
-      for (int u = a.m; u < s; ++u) acc += F[r * s + u] * Vj[u * s + col];
+      int col = c - a.mp;
+      for (int u = a.m; u < s; ++u) acc += F[r * s + u] * Vj[u * take + col];
     }
     M5[e] = (T)acc;
   }
@@ -733,7 +788,7 @@ struct Lobpcg {
   int64_t n;
   int m, mp, ld;
   int grid_pass;
-  DBuf<T> S, AS, bw, prec, M, tmpblk;
+  DBuf<T> S, AS, bw, prec, M, tmpblk, Wc;  // Wc: compact n x mp copy of W (SpMM input)
   DBuf<double> part0, part1, Gr0, Gr1, theta, colpart, colred, scratch;
   DBuf<int> status;
   double anorm = 0, bmax = 0, ydenom = 0;
@@ -744,6 +799,9 @@ struct Lobpcg {
     m = s.k;
     mp = (m + VN - 1) / VN * VN;
     ld = 3 * mp + VN;
+    // odd number of 16-byte chunks per row: 128-bit shared-memory loads of
+    // the same column from consecutive rows then hit distinct bank groups
+    if ((ld / VN) % 2 == 0) ld += VN;
   }
 
   size_t pass_smem(int ow) const {
@@ -852,7 +910,7 @@ struct Lobpcg {
     size_t sm = (size_t)R * 2 * mp * sizeof(double);
     k_resid<T><<<nb, bs, sm, ctx->stream>>>(n, S.p, AS.p, ld, m, mp, 2 * mp, theta.p, bw.p,
                                             sp.jacobi ? prec.p : nullptr, write_w ? S.p : nullptr,
-                                            colpart.p);
+                                            colpart.p, Wc.p);
     MG_CHECK_LAUNCH(ctx);
     k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, nb, 2 * mp, colred.p);
     MG_CHECK_LAUNCH(ctx);
@@ -1013,7 +1071,7 @@ struct Lobpcg {
     size_t sm = (size_t)R * 2 * mp * sizeof(double);
     k_resid<T><<<nb, bs, sm, ctx->stream>>>(n, S.p, AS.p, ld, m, mp, 2 * mp, theta.p, bw.p,
                                             sp.jacobi ? prec.p : nullptr, write_w ? S.p : nullptr,
-                                            colpart.p);
+                                            colpart.p, Wc.p);
     MG_CHECK_LAUNCH(ctx);
     k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, nb, 2 * mp, colred.p);
     MG_CHECK_LAUNCH(ctx);
@@ -1035,36 +1093,80 @@ struct Lobpcg {
 
   // ---- fast path (prefix iterations): one Gram pass + fused update/residual
   bool fast_ok = false;
-  int grid_fast = 0;
+  int grid_fast = 0, grid_upd = 0;
   size_t gram2_smem = 0, upd_smem = 0, fast_smem = 0;
   int fast_global = 0;
   DBuf<double> gpart;
   int64_t fast_steps = 0, fast_fallbacks = 0;
 
+  int tk_gram = 32, ns_gram = 3, tk_upd = 32, rt_upd = 8;
+
+  size_t gram2_bytes(int tk, int ns) const {
+    return (size_t)ns * (2 * ((size_t)tk * ld + 16) + tk + 16) * sizeof(T) + 16 + 64 +
+           (size_t)64 * kFThreads * sizeof(double) + 64;
+  }
+  size_t upd_bytes(int tk, int ns) const {
+    const int w = 3 * mp;
+    const size_t mlen = (size_t)w * mp + (size_t)mp * mp;
+    return (size_t)ns * (2 * ((size_t)tk * ld + 16) + tk + 16) * sizeof(T) +
+           (mlen + 16 + 4 * (size_t)tk * mp + mp + 4 + tk + 4) * sizeof(T) + 16 + 64 +
+           (size_t)kFThreads * 2 * sizeof(double) + 64;
+  }
+
   void fast_setup() {
     const char *env = getenv("MG_FAST");
     if (env && env[0] == '0') return;
-    const int w = 3 * mp;
-    const size_t tile_elems = (size_t)kFTK * ld + 16;
-    const size_t stage = (2 * tile_elems + kFTK + 16) * sizeof(T);
-    gram2_smem = 3 * stage + 64 + 64 + (size_t)64 * kFThreads * sizeof(double) + 128;
-    const size_t mlen = (size_t)w * mp + (size_t)mp * mp;
-    upd_smem = 2 * stage + (mlen + 16 + 4 * kFTK * mp + mp + 4 + kFTK + 4) * sizeof(T) + 64 + 64 +
-               (size_t)kFThreads * 2 * sizeof(double) + 128;
-    if (gram2_smem > 225 * 1024 || upd_smem > 225 * 1024 || m > 64) return;
+    if (m > 64) return;
+    const size_t budget = 225 * 1024;
+    // Gram pass: deepest ring (4, else 3 stages) of the tallest tiles that fit
+    ns_gram = 0;
+    for (int ns : {4, 3}) {
+      for (int tk = 256; tk >= 8; tk -= 8)
+        if (gram2_bytes(tk, ns) <= budget) {
+          tk_gram = tk;
+          ns_gram = ns;
+          break;
+        }
+      if (ns_gram && tk_gram >= 32) break;
+    }
+    if (!ns_gram) return;
+    tk_upd = 0;
+    for (int tk = 128; tk >= 8; tk -= 8)
+      if (upd_bytes(tk, 3) <= budget) {
+        tk_upd = tk;
+        break;
+      }
+    if (!tk_upd) return;
+    const int cb = (mp + 3) / 4;
+    rt_upd = 2;
+    for (int rt : {8, 4, 2})
+      if (tk_upd % rt == 0 && 2 * (tk_upd / rt) * cb >= kFThreads) {
+        rt_upd = rt;
+        break;
+      }
+    gram2_smem = gram2_bytes(tk_gram, ns_gram);
+    upd_smem = upd_bytes(tk_upd, 3);
     int smax = m + 2 * m;
     size_t need = (size_t)2 * std::max(smax * smax, 4 * m * m) * sizeof(double);
     fast_global = need > 190 * 1024;
     fast_smem = fast_global ? 0 : need;
     MG_CUDA(cudaFuncSetAttribute(k_gram2<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)gram2_smem));
-    MG_CUDA(cudaFuncSetAttribute(k_update_resid<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)upd_smem));
+                                 (int)gram2_bytes(tk_gram, 3)));
+    MG_CUDA(cudaFuncSetAttribute(k_gram2<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)budget));
+    MG_CUDA(cudaFuncSetAttribute(k_update_resid<T, 3, 8>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget));
+    MG_CUDA(cudaFuncSetAttribute(k_update_resid<T, 3, 4>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget));
+    MG_CUDA(cudaFuncSetAttribute(k_update_resid<T, 3, 2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget));
     if (fast_smem > 48 * 1024)
       MG_CUDA(cudaFuncSetAttribute(k_ctrl_fast<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)fast_smem));
-    int64_t ntile = (n + kFTK - 1) / kFTK;
+    int64_t ntile = (n + tk_gram - 1) / tk_gram;
     grid_fast = (int)std::min<int64_t>(ntile, ctx->num_sms);
+    grid_upd = (int)std::min<int64_t>((n + tk_upd - 1) / tk_upd, ctx->num_sms);
+    const int w = 3 * mp;
     gpart.alloc(ctx, (size_t)grid_fast * 2 * w * w);
     fast_ok = true;
   }
@@ -1075,6 +1177,7 @@ struct Lobpcg {
     const int w = 3 * mp;
     Gram2Args ga{};
     ga.n = n;
+    ga.tk = tk_gram;
     ga.ld = ld;
     ga.w = w;
     ga.nb = (w + 7) / 8;
@@ -1086,7 +1189,10 @@ struct Lobpcg {
       for (int lo = 0; lo < total; lo += kFThreads) {
         ga.blk_lo = lo;
         ga.nbr = std::min(kFThreads, total - lo);
-        k_gram2<T, 3><<<grid_fast, kFThreads, gram2_smem, ctx->stream>>>(S.p, AS.p, bw.p, ga);
+        if (ns_gram == 4)
+          k_gram2<T, 4><<<grid_fast, kFThreads, gram2_smem, ctx->stream>>>(S.p, AS.p, bw.p, ga);
+        else
+          k_gram2<T, 3><<<grid_fast, kFThreads, gram2_smem, ctx->stream>>>(S.p, AS.p, bw.p, ga);
         MG_CHECK_LAUNCH(ctx);
       }
     }
@@ -1106,6 +1212,13 @@ struct Lobpcg {
     fa.rel_tol = rel_tol();
     fa.abs_tol = sizeof(T) == 8 ? 1e-12 : 1e-7;
     fa.use_global = fast_global;
+    static int dbg_ctrl = -1;
+    if (dbg_ctrl < 0) {
+      const char *e = getenv("MG_DEBUG_CTRL");
+      dbg_ctrl = (e && e[0] == '1') ? 1 : 0;
+    }
+    const size_t clk_off = (size_t)11 * (3 * mp + VN) * (3 * mp + VN) + 4096;
+    fa.clk_off = dbg_ctrl ? (int)clk_off : 0;
     {
       ProfScope ps(ctx, PROF_CTRL, 0.0);
       k_ctrl_fast<T><<<1, 512, fast_smem, ctx->stream>>>(fa, Gr0.p, Gr1.p, M.p, theta.p, status.p,
@@ -1114,19 +1227,38 @@ struct Lobpcg {
     }
     UpdArgs ua{};
     ua.n = n;
+    ua.tk = tk_upd;
     ua.ld = ld;
     ua.w = w;
     ua.m = m;
     ua.mp = mp;
     ua.skip = status.p + 5;
+    ua.wc = Wc.p;
     ua.part = colpart.p;
     {
       ProfScope ps(ctx, PROF_UPDATE, 2.0 * n * ld * sizeof(T) + 5.0 * n * mp * sizeof(T));
-      k_update_resid<T, 2><<<grid_fast, kFThreads, upd_smem, ctx->stream>>>(
-          S.p, AS.p, bw.p, sp.jacobi ? prec.p : nullptr, M.p, theta.p, ua);
+      const T *pr = sp.jacobi ? prec.p : nullptr;
+      if (rt_upd == 8)
+        k_update_resid<T, 3, 8><<<grid_upd, kFThreads, upd_smem, ctx->stream>>>(S.p, AS.p, bw.p,
+                                                                               pr, M.p, theta.p, ua);
+      else if (rt_upd == 4)
+        k_update_resid<T, 3, 4><<<grid_upd, kFThreads, upd_smem, ctx->stream>>>(S.p, AS.p, bw.p,
+                                                                               pr, M.p, theta.p, ua);
+      else
+        k_update_resid<T, 3, 2><<<grid_upd, kFThreads, upd_smem, ctx->stream>>>(S.p, AS.p, bw.p,
+                                                                               pr, M.p, theta.p, ua);
       MG_CHECK_LAUNCH(ctx);
     }
-    k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, grid_fast, 2 * mp, colred.p);
+    if (dbg_ctrl && (iter_now % 50) == 1) {
+      long long clk[32];
+      d2h_sync(ctx, clk, scratch.p + clk_off, sizeof(clk));
+      fprintf(stderr, "[ctrl m=%d nv=%d it=%d] phases (kcycles):", m, fa.nv, iter_now);
+      for (int q = 1; q < 9; ++q) fprintf(stderr, " %.1f", (clk[q] - clk[q - 1]) / 1e3);
+      fprintf(stderr, " | eig:");
+      for (int q = 21; q < 26; ++q) fprintf(stderr, " %.1f", (clk[q] - clk[q - 1]) / 1e3);
+      fprintf(stderr, "\n");
+    }
+    k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, grid_upd, 2 * mp, colred.p);
     MG_CHECK_LAUNCH(ctx);
     MG_CUDA(cudaMemcpyAsync(colred.p + 2 * mp, theta.p, mp * sizeof(double),
                             cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1188,6 +1320,8 @@ struct Lobpcg {
     bw.alloc(ctx, n);
     prec.alloc(ctx, n);
     tmpblk.alloc(ctx, n * mp);
+    Wc.alloc(ctx, n * mp);
+    Wc.zero();
     int g = grid_for(n, 256, ctx->num_sms * 16);
     k_vec_T<T><<<g, 256, 0, ctx->stream>>>(n, b_dev, bw.p, 0);
     MG_CHECK_LAUNCH(ctx);
@@ -1203,7 +1337,7 @@ struct Lobpcg {
     theta.zero();
     colpart.alloc(ctx, (size_t)ctx->num_sms * 4 * 2 * wmax);
     colred.alloc(ctx, 4 * wmax + 8);
-    scratch.alloc(ctx, (size_t)8 * wmax * wmax + 4096);
+    scratch.alloc(ctx, (size_t)12 * wmax * wmax + 8192);
     status.alloc(ctx, 8);
     status.zero();
     size_t smax_pass = pass_smem(3 * mp);
@@ -1260,14 +1394,20 @@ struct Lobpcg {
       std::vector<int> vcols;
       for (int c = 0; c < m; ++c)
         if (!cv[c]) vcols.push_back(2 * mp + c);
-      deflate_cols(2 * mp, 3 * mp, 2 * mp, mp);
+      if (have_y) {
+        deflate_cols(2 * mp, 3 * mp, 2 * mp, mp);
+        k_copy_cols<T><<<grid_for(n * mp, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+            n, S.p, ld, 2 * mp, Wc.p, mp, 0, mp);
+        MG_CHECK_LAUNCH(ctx);
+      }
       const bool prefix = (it % 32) != 0;
       if (sizeof(T) == 4 && (it % refresh_period()) == 0) {
         // fp32: carried A-images drift at fp32 resolution; refresh [AX AP AW]
         // with one wide SpMM at every full re-orthonormalisation
         spmm_cols(0, 3 * mp);
       } else {
-        spmm_cols(2 * mp, mp);
+        spmm<T>(ctx, A, Wc.p, mp, AS.p + 2 * mp, ld, mp);  // compact W: L2-resident gathers
+        debug_check("spmm");
       }
       for (int c = 0; c < pcount; ++c) vcols.push_back(mp + c);
       bool done = false;

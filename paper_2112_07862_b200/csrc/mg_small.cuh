@@ -103,7 +103,10 @@ __device__ inline void blk_jacobi(double *A, int lda, int n, double *V, int ldv,
   }
   double fro = sqrt(red[0]);
   __syncthreads();
-  double abs_floor = 1e-3 * DBL_EPSILON * fro;
+  // rotate only couplings that can still move an eigenvalue by more than
+  // ~eps*||A||_F (absolute accuracy, like LAPACK syevd); relative criterion
+  // below it would force extra sweeps for the tiny Ritz values
+  double abs_floor = 0.25 * DBL_EPSILON * fro;
   int np = (n + 1) & ~1;  // even player count; player n (if odd) is a bye
   int half = np / 2;
   for (int sweep = 0; sweep < 60 && n > 1; ++sweep) {
