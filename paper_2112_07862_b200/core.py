@@ -646,6 +646,8 @@ def embed_arrays(n, indptr, indices, weights, k, cfg: SolverConfig | None = None
     cfg = cfg or SolverConfig(k=k + 1)
     s = _cfg_struct(cfg, k=k + 1)
     s.reserved = 1  # full K+1 vectors/eigenvalues
+    import os
+    s.reorder = 0 if os.environ.get("MG_REORDER", "1") == "0" else 1
     m = k + 1
     if device_inputs is None:
         p, i, w = _dev(indptr, torch.int64), _dev(indices, torch.int64), _dev(weights, torch.float64)

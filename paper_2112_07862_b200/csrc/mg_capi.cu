@@ -94,8 +94,10 @@ struct SolverIn {
 
 static SolveResult run_lobpcg(mg_ctx *ctx, const SolverIn &a, const double *b,
                               const mg_solver_cfg &cfg, const double *normals, int64_t n_normals,
-                              const double *deflate, double *eigvecs) {
+                              const double *deflate, double *eigvecs,
+                              const int64_t *perm = nullptr) {
   SolveSpec sp;
+  sp.perm = perm;
   sp.k = cfg.k;
   sp.max_iter = cfg.max_iter;
   sp.tol = cfg.tol;
@@ -133,7 +135,8 @@ static void check_b(mg_ctx *ctx, const double *b, int64_t n) {
 // smallest_above_null (eigensolver.py:431-460)
 static double smallest_above_null_impl(mg_ctx *ctx, const SolverIn &q, double tau, double tol,
                                        int max_iter, const double *normals, int64_t n_normals,
-                                       int precision, int *iters_out) {
+                                       int precision, int *iters_out,
+                                       const int64_t *perm = nullptr) {
   const int64_t n = q.n;
   if (n <= 512) {
     std::vector<double> w(n);
@@ -157,7 +160,7 @@ static double smallest_above_null_impl(mg_ctx *ctx, const SolverIn &q, double ta
     cfg.preconditioner = 1;
     cfg.precision = precision;
     DBuf<double> vecs(ctx, n * cfg.k);
-    SolveResult r = run_lobpcg(ctx, q, ones.p, cfg, normals, n_normals, cvec.p, vecs.p);
+    SolveResult r = run_lobpcg(ctx, q, ones.p, cfg, normals, n_normals, cvec.p, vecs.p, perm);
     if (iters_out) *iters_out += r.iterations;
     for (double v : r.eigenvalues)
       if (v > tau) return v;
@@ -168,14 +171,23 @@ static double smallest_above_null_impl(mg_ctx *ctx, const SolverIn &q, double ta
 
 // identity_shift (operators.py:138-156)
 static double identity_shift_impl(mg_ctx *ctx, const SolverIn &q, const double *normals,
-                                  int64_t n_normals, int precision, int *iters_out) {
+                                  int64_t n_normals, int precision, int *iters_out,
+                                  const int64_t *perm = nullptr) {
   if (iters_out) *iters_out = 0;
   require(check_symmetric(ctx, q.n, q.ptr, q.idx, q.data, 1e-12), MG_ERR_INPUT,
           "matrix is not symmetric");
   const int64_t n = q.n;
   if (n == 0 || q.nnz == 0) return 0.0;
   double tau = 1e-8 * trace(ctx, n, q.ptr, q.idx, q.data) / (double)n;
-  return smallest_above_null_impl(ctx, q, tau, 1e-6, 60, normals, n_normals, precision, iters_out);
+  return smallest_above_null_impl(ctx, q, tau, 1e-6, 60, normals, n_normals, precision, iters_out,
+                                  perm);
+}
+
+__global__ void k_scatter_rows(int64_t n, const double *__restrict__ src,
+                               const int64_t *__restrict__ perm, double *__restrict__ dst) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    dst[perm[r]] = src[r];
 }
 
 __global__ void k_drop_first_col(int64_t n, int K, const double *__restrict__ src,
@@ -232,6 +244,23 @@ static int embed_impl(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t 
     }
   }
   int64_t gnnz = nnz_of(ctx, ptr, n);
+  // locality order for the solver: relabel the graph once, map results back
+  DBuf<int64_t> perm, inv, pptr, pidx;
+  DBuf<double> pw;
+  const int64_t *perm_p = nullptr;
+  if (cfg.reorder && n > 4096) {
+    perm.alloc(ctx, n);
+    inv.alloc(ctx, n);
+    cm_order(ctx, n, ptr, idx, perm.p, inv.p);
+    pptr.alloc(ctx, n + 1);
+    pidx.alloc(ctx, gnnz > 0 ? gnnz : 1);
+    pw.alloc(ctx, gnnz > 0 ? gnnz : 1);
+    permute_graph(ctx, n, ptr, idx, w, perm.p, inv.p, pptr.p, pidx.p, pw.p);
+    ptr = pptr.p;
+    idx = pidx.p;
+    w = pw.p;
+    perm_p = perm.p;
+  }
   // L (graph.py:321-346)
   DBuf<int64_t> lptr(ctx, n + 1), lidx(ctx, gnnz + n);
   DBuf<double> ldata(ctx, gnnz + n);
@@ -253,7 +282,7 @@ static int embed_impl(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t 
   // eps (operators.py:138-156)
   SolverIn qin{n, qptr.p, qidx.p, qdata.p, qnnz};
   int eps_it = 0;
-  double eps = identity_shift_impl(ctx, qin, normals, n_normals, cfg.precision, &eps_it);
+  double eps = identity_shift_impl(ctx, qin, normals, n_normals, cfg.precision, &eps_it, perm_p);
   double t2 = now_s();
   double mu = repulsion_weight(ctx, n, qptr.p, qidx.p, qdata.p, eps);
   DBuf<int64_t> aptr(ctx, n + 1);
@@ -268,14 +297,25 @@ static int embed_impl(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t 
   qidx.release();
   qdata.release();
   double gdeg = 0;
-  int64_t bad = degree_balancing(ctx, n, aptr.p, aidx.p, adata.p, b_out, &gdeg);
+  DBuf<double> bperm;
+  double *b_solver = b_out;
+  if (perm_p) {
+    bperm.alloc(ctx, n);
+    b_solver = bperm.p;
+  }
+  int64_t bad = degree_balancing(ctx, n, aptr.p, aidx.p, adata.p, b_solver, &gdeg, perm_p);
   if (bad >= 0)
     throw Error(MG_ERR_DISCONNECTED, "node " + std::to_string(bad) +
                                          " has no off-diagonal coupling; extract the largest "
                                          "connected component and retry");
   double minleft;
   int64_t brow;
-  disc_left_min(ctx, n, aptr.p, aidx.p, adata.p, &minleft, &brow);
+  disc_left_min(ctx, n, aptr.p, aidx.p, adata.p, &minleft, &brow, perm_p);
+  if (perm_p) {  // b in the caller's node order
+    k_scatter_rows<<<grid_for(n, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(n, b_solver,
+                                                                                perm_p, b_out);
+    MG_CHECK_LAUNCH(ctx);
+  }
   d.mu = mu;
   d.epsilon = eps;
   d.min_disc_left_end = minleft;
@@ -287,7 +327,7 @@ static int embed_impl(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t 
   // solve K+1 pairs and drop the first (embedding.py:61-74, 94-103)
   DBuf<double> vecs(ctx, n * (int64_t)cfg.k);
   SolverIn ain{n, aptr.p, aidx.p, adata.p, annz};
-  SolveResult r = run_lobpcg(ctx, ain, b_out, cfg, normals, n_normals, nullptr, vecs.p);
+  SolveResult r = run_lobpcg(ctx, ain, b_solver, cfg, normals, n_normals, nullptr, vecs.p, perm_p);
   const bool full = cfg_in->reserved == 1;  // caller wants all K+1 pairs (drop done by caller)
   if (full) {
     MG_CUDA(cudaMemcpyAsync(P, vecs.p, n * (int64_t)cfg.k * sizeof(double),

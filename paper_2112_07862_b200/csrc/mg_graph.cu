@@ -73,11 +73,12 @@ __device__ __forceinline__ VI vi_min(VI a, VI b) {
 }
 
 __global__ void k_partial_argmin(const double *__restrict__ x, int64_t n, int64_t chunk,
-                                 VI *__restrict__ part) {
+                                 VI *__restrict__ part, const int64_t *__restrict__ imap) {
   __shared__ VI sm[kBlock];
   int64_t lo = (int64_t)blockIdx.x * chunk, hi = min(n, lo + chunk);
   VI best{INFINITY, LLONG_MAX};
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) best = vi_min(best, VI{x[i], i});
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+    best = vi_min(best, VI{x[i], imap ? imap[i] : i});
   sm[threadIdx.x] = best;
   __syncthreads();
   for (int o = kBlock / 2; o > 0; o >>= 1) {
@@ -100,11 +101,11 @@ __global__ void k_final_argmin(const VI *__restrict__ part, int np, VI *out) {
   if (threadIdx.x == 0) *out = sm[0];
 }
 
-static VI argmin_f64(mg_ctx *ctx, const double *x, int64_t n) {
+static VI argmin_f64(mg_ctx *ctx, const double *x, int64_t n, const int64_t *imap = nullptr) {
   int nb = grid_for(n, kBlock * 8, 1024);
   int64_t chunk = (n + nb - 1) / nb;
   DBuf<VI> part(ctx, nb + 1);
-  k_partial_argmin<<<nb, kBlock, 0, ctx->stream>>>(x, n, chunk, part.p);
+  k_partial_argmin<<<nb, kBlock, 0, ctx->stream>>>(x, n, chunk, part.p, imap);
   MG_CHECK_LAUNCH(ctx);
   k_final_argmin<<<1, kBlock, 0, ctx->stream>>>(part.p, nb, part.p + nb);
   MG_CHECK_LAUNCH(ctx);
@@ -717,7 +718,8 @@ void assemble_fill(mg_ctx *ctx, int64_t n, const int64_t *lptr, const int64_t *l
 // two mean passes).
 __global__ void k_radii(int64_t n, const int64_t *__restrict__ ptr, const int64_t *__restrict__ idx,
                         const double *__restrict__ data, double *__restrict__ radius,
-                        double *__restrict__ left, unsigned long long *first_bad) {
+                        double *__restrict__ left, unsigned long long *first_bad,
+                        const int64_t *__restrict__ perm) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double r = 0.0, d = 0.0;
@@ -727,7 +729,7 @@ __global__ void k_radii(int64_t n, const int64_t *__restrict__ ptr, const int64_
     }
     if (radius) radius[i] = r;
     if (left) left[i] = __dsub_rn(d, r);
-    if (first_bad && !(r > 0.0)) atomicMin(first_bad, (unsigned long long)i);
+    if (first_bad && !(r > 0.0)) atomicMin(first_bad, (unsigned long long)(perm ? perm[i] : i));
   }
 }
 
@@ -752,7 +754,7 @@ __global__ void k_exp_sub(double *__restrict__ b, const double *__restrict__ x, 
 }
 
 int64_t degree_balancing(mg_ctx *ctx, int64_t n, const int64_t *aptr, const int64_t *aidx,
-                         const double *adata, double *b, double *gdeg) {
+                         const double *adata, double *b, double *gdeg, const int64_t *perm) {
   if (n == 0) {
     *gdeg = NAN;
     return -1;
@@ -761,7 +763,7 @@ int64_t degree_balancing(mg_ctx *ctx, int64_t n, const int64_t *aptr, const int6
   DBuf<unsigned long long> bad(ctx, 1);
   MG_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), ctx->stream));
   int g = grid_for(n, kBlock, ctx->num_sms * 16);
-  k_radii<<<g, kBlock, 0, ctx->stream>>>(n, aptr, aidx, adata, rad.p, nullptr, bad.p);
+  k_radii<<<g, kBlock, 0, ctx->stream>>>(n, aptr, aidx, adata, rad.p, nullptr, bad.p, perm);
   MG_CHECK_LAUNCH(ctx);
   unsigned long long first;
   d2h_sync(ctx, &first, bad.p, sizeof(first));
@@ -779,7 +781,7 @@ int64_t degree_balancing(mg_ctx *ctx, int64_t n, const int64_t *aptr, const int6
 }
 
 void disc_left_min(mg_ctx *ctx, int64_t n, const int64_t *aptr, const int64_t *aidx,
-                   const double *adata, double *min_left, int64_t *row) {
+                   const double *adata, double *min_left, int64_t *row, const int64_t *perm) {
   if (n == 0) {
     *min_left = NAN;
     *row = 0;
@@ -787,9 +789,9 @@ void disc_left_min(mg_ctx *ctx, int64_t n, const int64_t *aptr, const int64_t *a
   }
   DBuf<double> left(ctx, n);
   k_radii<<<grid_for(n, kBlock, ctx->num_sms * 16), kBlock, 0, ctx->stream>>>(
-      n, aptr, aidx, adata, nullptr, left.p, nullptr);
+      n, aptr, aidx, adata, nullptr, left.p, nullptr, nullptr);
   MG_CHECK_LAUNCH(ctx);
-  VI r = argmin_f64(ctx, left.p, n);
+  VI r = argmin_f64(ctx, left.p, n, perm);
   *min_left = r.v;
   *row = r.i;
 }

@@ -26,11 +26,21 @@ void assemble_fill(mg_ctx *ctx, int64_t n, const int64_t *lptr, const int64_t *l
                    const double *ldata, const int64_t *qptr, const int64_t *qidx,
                    const double *qdata, double mu, double eps, const int64_t *aptr,
                    int64_t *aidx, double *adata);
-// returns -1 on success, else the first isolated row (b untouched)
+// returns -1 on success, else the first isolated row (b untouched).  With
+// `perm` (row r is original node perm[r]) the reported row and every
+// first-index tie-break use original ids.
 int64_t degree_balancing(mg_ctx *ctx, int64_t n, const int64_t *aptr, const int64_t *aidx,
-                         const double *adata, double *b, double *gdeg);
+                         const double *adata, double *b, double *gdeg,
+                         const int64_t *perm = nullptr);
 void disc_left_min(mg_ctx *ctx, int64_t n, const int64_t *aptr, const int64_t *aidx,
-                   const double *adata, double *min_left, int64_t *row);
+                   const double *adata, double *min_left, int64_t *row,
+                   const int64_t *perm = nullptr);
+// Cuthill-McKee locality order (mg_reorder.cu): perm new->old, inv old->new
+void cm_order(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *idx, int64_t *perm,
+              int64_t *inv);
+void permute_graph(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *idx, const double *w,
+                   const int64_t *perm, const int64_t *inv, int64_t *nptr, int64_t *nidx,
+                   double *nw);
 double trace(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *idx, const double *data);
 // dense eigenvalues (ascending) of a small CSR matrix, n <= 512 (operators.py:150-152)
 void dense_eigvals(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *idx,

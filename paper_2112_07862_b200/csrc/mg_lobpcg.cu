@@ -1138,9 +1138,10 @@ struct Lobpcg {
       }
     if (!tk_upd) return;
     const int cb = (mp + 3) / 4;
+    // tallest register block that still keeps >= 3/4 of the threads busy
     rt_upd = 2;
     for (int rt : {8, 4, 2})
-      if (tk_upd % rt == 0 && 2 * (tk_upd / rt) * cb >= kFThreads) {
+      if (tk_upd % rt == 0 && 2 * (tk_upd / rt) * cb >= (3 * kFThreads) / 4) {
         rt_upd = rt;
         break;
       }
