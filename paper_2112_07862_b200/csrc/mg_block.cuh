@@ -25,6 +25,11 @@ struct DevCSR {
   const int64_t *ptr = nullptr;
   const int *idx = nullptr;
   const T *val = nullptr;
+  // fp32 solver: row sums of the fp64 matrix.  A x is then evaluated in
+  // difference form  (A x)_i = sum_j A_ij (x_j - x_i) + r_i x_i : the fp32
+  // rounding of A_ij becomes a zero-row-sum perturbation whose effect scales
+  // with the eigenvalue instead of ||A|| (A and Q are Laplacian-like).
+  const T *rowsum = nullptr;
 };
 
 // Owning version (conversion from the reference's int64/f64 CSR).
@@ -33,6 +38,7 @@ struct OwnedCSR {
   DBuf<int64_t> ptr;
   DBuf<int> idx;
   DBuf<T> val;
+  DBuf<T> rowsum;
   DevCSR<T> view;
 };
 

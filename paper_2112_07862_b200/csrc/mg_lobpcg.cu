@@ -50,6 +50,17 @@ __global__ void k_csr_convert(int64_t nnz, const int64_t *__restrict__ idx,
 }
 
 template <typename T>
+__global__ void k_rowsum(int64_t n, const int64_t *__restrict__ ptr, const double *__restrict__ val,
+                         T *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) s += val[k];
+    out[i] = (T)s;
+  }
+}
+
+template <typename T>
 void make_solver_csr(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *idx,
                      const double *val, OwnedCSR<T> &out, int64_t nnz_hint) {
   int64_t nnz = nnz_hint;
@@ -69,6 +80,15 @@ void make_solver_csr(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *
   out.view.ptr = out.ptr.p;
   out.view.idx = out.idx.p;
   out.view.val = out.val.p;
+  out.view.rowsum = nullptr;
+  const char *env = getenv("MG_SPMM_DIFF");
+  if (sizeof(T) == 4 && !(env && env[0] == '0')) {
+    out.rowsum.alloc(ctx, n > 0 ? n : 1);
+    k_rowsum<T><<<grid_for(n, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(n, ptr, val,
+                                                                              out.rowsum.p);
+    MG_CHECK_LAUNCH(ctx);
+    out.view.rowsum = out.rowsum.p;
+  }
 }
 
 // ------------------------------------------------------------------ SpMM ---
@@ -123,11 +143,11 @@ __device__ __forceinline__ double2 ld_keep(const double2 *a, uint64_t pol) {
   return v;
 }
 
-template <typename T>
+template <typename T, bool DIFF>
 __global__ void __launch_bounds__(256)
     k_spmm(int64_t n, const int64_t *__restrict__ ptr, const int *__restrict__ idx,
            const T *__restrict__ val, const T *__restrict__ X, int ldx, T *__restrict__ Y, int ldy,
-           int L) {
+           int L, const T *__restrict__ rowsum) {
   using V = typename VecT<T>::V;
   constexpr int VN = VecT<T>::N;
   int lane = threadIdx.x & 31;
@@ -139,9 +159,15 @@ __global__ void __launch_bounds__(256)
   int64_t stride = (int64_t)gridDim.x * per_block;
   for (int64_t row = blockIdx.x * per_block + (threadIdx.x >> 5) * G + g; row < n; row += stride) {
     int64_t s = ptr[row], e = ptr[row + 1];
-    T acc[VN];
+    T acc[VN], xi[VN];
 #pragma unroll
     for (int q = 0; q < VN; ++q) acc[q] = T(0);
+    if (DIFF) {
+      V xs = ld_keep(reinterpret_cast<const V *>(X + row * (int64_t)ldx) + gl, pl);
+      const T *ps = reinterpret_cast<const T *>(&xs);
+#pragma unroll
+      for (int q = 0; q < VN; ++q) xi[q] = ps[q];
+    }
     int64_t k = s;
     for (; k + 4 <= e; k += 4) {
       int j0 = ld_stream_i32(idx + k, pf), j1 = ld_stream_i32(idx + k + 1, pf),
@@ -154,12 +180,22 @@ __global__ void __launch_bounds__(256)
       V x3 = ld_keep(reinterpret_cast<const V *>(X + (int64_t)j3 * ldx) + gl, pl);
       const T *p0 = reinterpret_cast<const T *>(&x0), *p1 = reinterpret_cast<const T *>(&x1),
               *p2 = reinterpret_cast<const T *>(&x2), *p3 = reinterpret_cast<const T *>(&x3);
+      if (DIFF) {
 #pragma unroll
-      for (int q = 0; q < VN; ++q) {
-        acc[q] += v0 * p0[q];
-        acc[q] += v1 * p1[q];
-        acc[q] += v2 * p2[q];
-        acc[q] += v3 * p3[q];
+        for (int q = 0; q < VN; ++q) {
+          acc[q] += v0 * (p0[q] - xi[q]);
+          acc[q] += v1 * (p1[q] - xi[q]);
+          acc[q] += v2 * (p2[q] - xi[q]);
+          acc[q] += v3 * (p3[q] - xi[q]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < VN; ++q) {
+          acc[q] += v0 * p0[q];
+          acc[q] += v1 * p1[q];
+          acc[q] += v2 * p2[q];
+          acc[q] += v3 * p3[q];
+        }
       }
     }
     for (; k < e; ++k) {
@@ -168,7 +204,12 @@ __global__ void __launch_bounds__(256)
       V x0 = ld_keep(reinterpret_cast<const V *>(X + (int64_t)j0 * ldx) + gl, pl);
       const T *p0 = reinterpret_cast<const T *>(&x0);
 #pragma unroll
-      for (int q = 0; q < VN; ++q) acc[q] += v0 * p0[q];
+      for (int q = 0; q < VN; ++q) acc[q] += DIFF ? v0 * (p0[q] - xi[q]) : v0 * p0[q];
+    }
+    if (DIFF) {
+      const T rs = rowsum[row];
+#pragma unroll
+      for (int q = 0; q < VN; ++q) acc[q] += rs * xi[q];
     }
     V out;
     T *po = reinterpret_cast<T *>(&out);
@@ -190,7 +231,12 @@ void spmm(mg_ctx *ctx, const DevCSR<T> &A, const T *X, int ldx, T *Y, int ldy, i
   double bytes = (double)A.nnz * (sizeof(T) + sizeof(int)) + 8.0 * (A.n + 1) +
                  2.0 * sizeof(T) * (double)A.n * w;
   ProfScope ps(ctx, PROF_SPMM, bytes);
-  k_spmm<T><<<grid, 256, 0, ctx->stream>>>(A.n, A.ptr, A.idx, A.val, X, ldx, Y, ldy, L);
+  if (A.rowsum)
+    k_spmm<T, true><<<grid, 256, 0, ctx->stream>>>(A.n, A.ptr, A.idx, A.val, X, ldx, Y, ldy, L,
+                                                   A.rowsum);
+  else
+    k_spmm<T, false><<<grid, 256, 0, ctx->stream>>>(A.n, A.ptr, A.idx, A.val, X, ldx, Y, ldy, L,
+                                                    nullptr);
   MG_CHECK_LAUNCH(ctx);
 }
 
