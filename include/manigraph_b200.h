@@ -210,6 +210,41 @@ int mg_embed_host(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *
                   int32_t check_connected, const double *normals, int64_t n_normals,
                   double *P, double *b, mg_solver_out *out, mg_embed_diag *diag);
 
+/* ---------------------------------------------------- multi-GPU (8(e)) ---
+ * 1-D row partition of the solve over ranks (one process per GPU).  The
+ * setup (Q, eps, mu, A, b) is replicated; each LOBPCG SpMM exchanges halo
+ * rows (NCCL grouped send/recv) and every Gram / norm reduction is an NCCL
+ * allreduce of a small fp64 block.  The reference has no distributed mode
+ * (single-process numpy/scipy, eigensolver.py:165-283); results agree with
+ * mg_embed to the solver tolerance (reduction order differs). */
+typedef struct mg_comm mg_comm;
+int mg_nccl_unique_id(uint8_t *uid /* host 128 bytes */);
+int mg_comm_create_nccl(mg_ctx *ctx, int32_t nranks, int32_t rank, const uint8_t *uid,
+                        mg_comm **out);
+/* R virtual ranks as threads of one process (tests; collectives through the host) */
+int mg_local_group_create(int32_t nranks, void **group);
+int mg_local_group_destroy(void *group);
+int mg_comm_create_local(void *group, int32_t rank, mg_comm **out);
+int mg_comm_destroy(mg_comm *comm);
+/* mg_embed over the ranks of `comm`; every rank passes the full graph and
+ * receives the full P / b / diagnostics */
+int mg_embed_dist(mg_ctx *ctx, mg_comm *comm, int64_t n, const int64_t *indptr,
+                  const int64_t *indices, const double *weights, int32_t K,
+                  const mg_solver_cfg *cfg, int32_t literal_diagonal, int32_t require_convergence,
+                  int32_t check_connected, const double *normals, int64_t n_normals, double *P,
+                  double *b, mg_solver_out *out, mg_embed_diag *diag);
+/* halo plan of `rank` for a HOST CSR (no GPU needed): row range [r0, r0+nloc),
+ * sorted halo rows, per-peer receive/send offsets+counts (nranks each), local
+ * rows to send, and the local CSR's remapped column ids ([local | halo]).
+ * Output arrays may be NULL (query sizes via info first). */
+typedef struct mg_dist_plan_info {
+  int64_t r0, nloc, nhalo, nsend, local_nnz;
+} mg_dist_plan_info;
+int mg_dist_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices, int32_t nranks,
+                      int32_t rank, mg_dist_plan_info *info, int64_t *halo, int64_t *roff,
+                      int64_t *rcnt, int64_t *soff, int64_t *scnt, int32_t *send_rows,
+                      int32_t *local_indices);
+
 #ifdef __cplusplus
 }
 #endif

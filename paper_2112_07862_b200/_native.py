@@ -80,7 +80,21 @@ SIGNATURES = {
                  C.POINTER(SolverOut), C.POINTER(EmbedDiag)],
     "mg_embed_host": [vp, i64, vp, vp, vp, i32, C.POINTER(SolverCfg), i32, i32, i32, vp, i64,
                       vp, vp, C.POINTER(SolverOut), C.POINTER(EmbedDiag)],
+    # multi-GPU (row-partitioned solve)
+    "mg_nccl_unique_id": [vp],
+    "mg_comm_create_nccl": [vp, i32, i32, vp, C.POINTER(vp)],
+    "mg_local_group_create": [i32, C.POINTER(vp)],
+    "mg_local_group_destroy": [vp],
+    "mg_comm_create_local": [vp, i32, C.POINTER(vp)],
+    "mg_comm_destroy": [vp],
+    "mg_embed_dist": [vp, vp, i64, vp, vp, vp, i32, C.POINTER(SolverCfg), i32, i32, i32, vp, i64,
+                      vp, vp, C.POINTER(SolverOut), C.POINTER(EmbedDiag)],
+    "mg_dist_plan_host": [i64, vp, vp, i32, i32, C.c_void_p, vp, vp, vp, vp, vp, vp, vp],
 }
+
+
+class DistPlanInfo(C.Structure):
+    _fields_ = [("r0", i64), ("nloc", i64), ("nhalo", i64), ("nsend", i64), ("local_nnz", i64)]
 
 
 class NativeUnavailable(RuntimeError):

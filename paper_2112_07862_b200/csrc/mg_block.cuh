@@ -4,6 +4,7 @@
 #include "mg_common.cuh"
 
 namespace mg {
+struct Comm;
 
 template <typename T>
 struct VecT;
@@ -59,6 +60,12 @@ struct SolveSpec {
   int64_t n_normals = 0;
   const double *deflate = nullptr;  // device n (one vector) or null
   const int64_t *perm = nullptr;    // optional: solver row r is original row perm[r]
+  // distributed mode (mg_dist.cuh): communicator and this rank's DistPart<T>;
+  // rows are the global rows [row_base, row_base + n_local)
+  struct Comm *comm = nullptr;
+  const void *dist = nullptr;
+  int64_t row_base = 0;
+  int64_t n_global = 0;
 };
 
 struct SolveResult {

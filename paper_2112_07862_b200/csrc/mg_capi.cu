@@ -6,6 +6,8 @@
 #include <cmath>
 
 #include "mg_block.cuh"
+#include "mg_comm.cuh"
+#include "mg_dist.cuh"
 #include "mg_graph.cuh"
 #include "mg_small.cuh"
 
@@ -95,7 +97,7 @@ struct SolverIn {
 static SolveResult run_lobpcg(mg_ctx *ctx, const SolverIn &a, const double *b,
                               const mg_solver_cfg &cfg, const double *normals, int64_t n_normals,
                               const double *deflate, double *eigvecs,
-                              const int64_t *perm = nullptr) {
+                              const int64_t *perm = nullptr, Comm *comm = nullptr) {
   SolveSpec sp;
   sp.perm = perm;
   sp.k = cfg.k;
@@ -114,6 +116,29 @@ static SolveResult run_lobpcg(mg_ctx *ctx, const SolverIn &a, const double *b,
   k_diag_of<<<grid_for(a.n, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(a.n, a.ptr, a.idx,
                                                                             a.data, diag.p);
   MG_CHECK_LAUNCH(ctx);
+  if (comm && comm->nranks > 1) {
+    // 1-D row partition: the (replicated) matrix is cut into this rank's
+    // rows with halo columns; b, diag and the deflation vector are sliced
+    require(a.n < INT32_MAX, MG_ERR_INPUT, "distributed solve limited to n < 2^31");
+    require(a.n >= 4 * (int64_t)comm->nranks, MG_ERR_INPUT,
+            "distributed solve needs at least 4 rows per rank");
+    sp.comm = comm;
+    sp.n_global = a.n;
+    if (cfg.precision == 1) {
+      DistPart<float> dp;
+      build_dist<float>(ctx, comm, a.n, a.ptr, a.idx, a.data, dp);
+      sp.dist = &dp;
+      sp.row_base = dp.r0;
+      if (deflate) sp.deflate = deflate + dp.r0;
+      return lobpcg<float>(ctx, dp.A.view, anorm, b + dp.r0, diag.p + dp.r0, sp, eigvecs);
+    }
+    DistPart<double> dp;
+    build_dist<double>(ctx, comm, a.n, a.ptr, a.idx, a.data, dp);
+    sp.dist = &dp;
+    sp.row_base = dp.r0;
+    if (deflate) sp.deflate = deflate + dp.r0;
+    return lobpcg<double>(ctx, dp.A.view, anorm, b + dp.r0, diag.p + dp.r0, sp, eigvecs);
+  }
   if (cfg.precision == 1) {
     OwnedCSR<float> A;
     make_solver_csr<float>(ctx, a.n, a.ptr, a.idx, a.data, A, a.nnz);
@@ -136,7 +161,7 @@ static void check_b(mg_ctx *ctx, const double *b, int64_t n) {
 static double smallest_above_null_impl(mg_ctx *ctx, const SolverIn &q, double tau, double tol,
                                        int max_iter, const double *normals, int64_t n_normals,
                                        int precision, int *iters_out,
-                                       const int64_t *perm = nullptr) {
+                                       const int64_t *perm = nullptr, Comm *comm = nullptr) {
   const int64_t n = q.n;
   if (n <= 512) {
     std::vector<double> w(n);
@@ -160,7 +185,8 @@ static double smallest_above_null_impl(mg_ctx *ctx, const SolverIn &q, double ta
     cfg.preconditioner = 1;
     cfg.precision = precision;
     DBuf<double> vecs(ctx, n * cfg.k);
-    SolveResult r = run_lobpcg(ctx, q, ones.p, cfg, normals, n_normals, cvec.p, vecs.p, perm);
+    SolveResult r =
+        run_lobpcg(ctx, q, ones.p, cfg, normals, n_normals, cvec.p, vecs.p, perm, comm);
     if (iters_out) *iters_out += r.iterations;
     for (double v : r.eigenvalues)
       if (v > tau) return v;
@@ -172,7 +198,7 @@ static double smallest_above_null_impl(mg_ctx *ctx, const SolverIn &q, double ta
 // identity_shift (operators.py:138-156)
 static double identity_shift_impl(mg_ctx *ctx, const SolverIn &q, const double *normals,
                                   int64_t n_normals, int precision, int *iters_out,
-                                  const int64_t *perm = nullptr) {
+                                  const int64_t *perm = nullptr, Comm *comm = nullptr) {
   if (iters_out) *iters_out = 0;
   require(check_symmetric(ctx, q.n, q.ptr, q.idx, q.data, 1e-12), MG_ERR_INPUT,
           "matrix is not symmetric");
@@ -180,7 +206,7 @@ static double identity_shift_impl(mg_ctx *ctx, const SolverIn &q, const double *
   if (n == 0 || q.nnz == 0) return 0.0;
   double tau = 1e-8 * trace(ctx, n, q.ptr, q.idx, q.data) / (double)n;
   return smallest_above_null_impl(ctx, q, tau, 1e-6, 60, normals, n_normals, precision, iters_out,
-                                  perm);
+                                  perm, comm);
 }
 
 __global__ void k_scatter_rows(int64_t n, const double *__restrict__ src,
@@ -224,7 +250,8 @@ static void fill_out(const SolveResult &r, mg_solver_out *out, int k) {
 static int embed_impl(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *idx,
                       const double *w, int32_t K, const mg_solver_cfg *cfg_in, int literal,
                       int require_conv, int check_conn, const double *normals, int64_t n_normals,
-                      double *P, double *b_out, mg_solver_out *out, mg_embed_diag *diag) {
+                      double *P, double *b_out, mg_solver_out *out, mg_embed_diag *diag,
+                      Comm *comm = nullptr) {
   double t0 = now_s();
   mg_embed_diag d{};
   require(K >= 1 && K <= n - 1, MG_ERR_INPUT,
@@ -282,7 +309,8 @@ static int embed_impl(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t 
   // eps (operators.py:138-156)
   SolverIn qin{n, qptr.p, qidx.p, qdata.p, qnnz};
   int eps_it = 0;
-  double eps = identity_shift_impl(ctx, qin, normals, n_normals, cfg.precision, &eps_it, perm_p);
+  double eps =
+      identity_shift_impl(ctx, qin, normals, n_normals, cfg.precision, &eps_it, perm_p, comm);
   double t2 = now_s();
   double mu = repulsion_weight(ctx, n, qptr.p, qidx.p, qdata.p, eps);
   DBuf<int64_t> aptr(ctx, n + 1);
@@ -327,7 +355,8 @@ static int embed_impl(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t 
   // solve K+1 pairs and drop the first (embedding.py:61-74, 94-103)
   DBuf<double> vecs(ctx, n * (int64_t)cfg.k);
   SolverIn ain{n, aptr.p, aidx.p, adata.p, annz};
-  SolveResult r = run_lobpcg(ctx, ain, b_solver, cfg, normals, n_normals, nullptr, vecs.p, perm_p);
+  SolveResult r =
+      run_lobpcg(ctx, ain, b_solver, cfg, normals, n_normals, nullptr, vecs.p, perm_p, comm);
   const bool full = cfg_in->reserved == 1;  // caller wants all K+1 pairs (drop done by caller)
   if (full) {
     MG_CUDA(cudaMemcpyAsync(P, vecs.p, n * (int64_t)cfg.k * sizeof(double),
@@ -669,6 +698,97 @@ int mg_embed(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indic
   require(cfg != nullptr, MG_ERR_INPUT, "cfg is NULL");
   return embed_impl(ctx, n, indptr, indices, weights, K, cfg, literal_diagonal,
                     require_convergence, check_connected, normals, n_normals, P, b, out, diag);
+  MG_API_END
+}
+
+int mg_nccl_unique_id(uint8_t *uid) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(uid != nullptr, MG_ERR_INPUT, "uid is NULL");
+  nccl_unique_id(uid);
+  MG_API_END
+}
+
+int mg_comm_create_nccl(mg_ctx *ctx, int32_t nranks, int32_t rank, const uint8_t *uid,
+                        mg_comm **out) {
+  MG_API_BEGIN(ctx)
+  require(ctx && uid && out, MG_ERR_INPUT, "NULL argument");
+  require(nranks >= 1 && rank >= 0 && rank < nranks, MG_ERR_INPUT, "bad rank / world size");
+  auto *c = new mg_comm();
+  try {
+    c->impl = make_nccl_comm(nranks, rank, uid);
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  *out = c;
+  MG_API_END
+}
+
+int mg_local_group_create(int32_t nranks, void **group) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(nranks >= 1 && group, MG_ERR_INPUT, "bad arguments");
+  *group = local_comm_group_create(nranks);
+  MG_API_END
+}
+
+int mg_local_group_destroy(void *group) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  local_comm_group_destroy(group);
+  MG_API_END
+}
+
+int mg_comm_create_local(void *group, int32_t rank, mg_comm **out) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(group && out, MG_ERR_INPUT, "NULL argument");
+  auto *c = new mg_comm();
+  c->impl = local_comm_rank(group, rank);
+  *out = c;
+  MG_API_END
+}
+
+int mg_comm_destroy(mg_comm *comm) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  if (comm) {
+    delete comm->impl;
+    delete comm;
+  }
+  MG_API_END
+}
+
+int mg_embed_dist(mg_ctx *ctx, mg_comm *comm, int64_t n, const int64_t *indptr,
+                  const int64_t *indices, const double *weights, int32_t K,
+                  const mg_solver_cfg *cfg, int32_t literal_diagonal, int32_t require_convergence,
+                  int32_t check_connected, const double *normals, int64_t n_normals, double *P,
+                  double *b, mg_solver_out *out, mg_embed_diag *diag) {
+  MG_API_BEGIN(ctx)
+  require(cfg != nullptr && comm != nullptr, MG_ERR_INPUT, "cfg / comm is NULL");
+  return embed_impl(ctx, n, indptr, indices, weights, K, cfg, literal_diagonal,
+                    require_convergence, check_connected, normals, n_normals, P, b, out, diag,
+                    comm->impl);
+  MG_API_END
+}
+
+int mg_dist_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices, int32_t nranks,
+                      int32_t rank, mg_dist_plan_info *info, int64_t *halo, int64_t *roff,
+                      int64_t *rcnt, int64_t *soff, int64_t *scnt, int32_t *send_rows,
+                      int32_t *local_indices) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(indptr && indices && info, MG_ERR_INPUT, "NULL argument");
+  HostPlan hp;
+  std::vector<int> lidx;
+  host_plan(n, indptr, indices, nranks, rank, hp, local_indices ? &lidx : nullptr);
+  info->r0 = hp.r0;
+  info->nloc = hp.nloc;
+  info->nhalo = (int64_t)hp.halo.size();
+  info->nsend = (int64_t)hp.send_rows.size();
+  info->local_nnz = indptr[hp.r0 + hp.nloc] - indptr[hp.r0];
+  if (halo) std::copy(hp.halo.begin(), hp.halo.end(), halo);
+  if (roff) std::copy(hp.roff.begin(), hp.roff.end(), roff);
+  if (rcnt) std::copy(hp.rcnt.begin(), hp.rcnt.end(), rcnt);
+  if (soff) std::copy(hp.soff.begin(), hp.soff.end(), soff);
+  if (scnt) std::copy(hp.scnt.begin(), hp.scnt.end(), scnt);
+  if (send_rows) std::copy(hp.send_rows.begin(), hp.send_rows.end(), send_rows);
+  if (local_indices) std::copy(lidx.begin(), lidx.end(), local_indices);
   MG_API_END
 }
 

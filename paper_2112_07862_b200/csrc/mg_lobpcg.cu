@@ -28,6 +28,7 @@
 #include "mg_small.cuh"
 #include "mg_fastk.cuh"
 #include "mg_eig.cuh"
+#include "mg_dist.cuh"
 
 namespace mg {
 
@@ -306,7 +307,7 @@ __global__ void k_coldot(int64_t n, const T *__restrict__ S, const T *__restrict
 template <typename T>
 __global__ void k_colamax(int64_t n, const T *__restrict__ S, int ld, int mp,
                           const int64_t *__restrict__ perm, double *__restrict__ pv,
-                          int64_t *__restrict__ pi, double *__restrict__ pval) {
+                          int64_t *__restrict__ pi, double *__restrict__ pval, int64_t row_base) {
   extern __shared__ double sm_a[];
   int R = blockDim.x / mp;
   int c = threadIdx.x % mp, rr = threadIdx.x / mp;
@@ -316,7 +317,7 @@ __global__ void k_colamax(int64_t n, const T *__restrict__ S, int ld, int mp,
     for (int64_t row = (int64_t)blockIdx.x * R + rr; row < n; row += (int64_t)gridDim.x * R) {
       double x = (double)S[row * ld + c];
       double a = fabs(x);
-      int64_t oi = perm ? perm[row] : row;
+      int64_t oi = perm ? perm[row_base + row] : row_base + row;
       if (a > best || (a == best && oi < bi)) {
         best = a;
         bi = oi;
@@ -360,14 +361,27 @@ __global__ void k_reduce_cols(const double *__restrict__ part, int nb, int w,
 // X0 from the normal stream: S[r][c0 + c] = z[off + r*w + c]  (row-major (n, w))
 template <typename T>
 __global__ void k_load_normals(int64_t n, int w, const double *__restrict__ z, int64_t off,
-                               const int64_t *__restrict__ perm, T *__restrict__ S, int ld, int c0) {
+                               const int64_t *__restrict__ perm, T *__restrict__ S, int ld, int c0,
+                               int64_t row_base) {
   int64_t total = n * (int64_t)w;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = e / w;
     int c = (int)(e - r * w);
-    int64_t src = perm ? perm[r] : r;
+    int64_t src = perm ? perm[row_base + r] : row_base + r;
     S[r * ld + c0 + c] = (T)z[off + src * w + c];
+  }
+}
+
+template <typename T>
+__global__ void k_pack_rows(const T *__restrict__ X, int w, const int *__restrict__ rows,
+                            int64_t nrows, T *__restrict__ out) {
+  int64_t total = nrows * (int64_t)w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / w;
+    int c = (int)(e - r * w);
+    out[e] = X[(int64_t)rows[r] * w + c];
   }
 }
 
@@ -395,13 +409,14 @@ __global__ void k_copy_cols(int64_t n, const T *__restrict__ src, int lds, int s
 template <typename T>
 __global__ void k_write_vectors(int64_t n, const T *__restrict__ S, int ld, int k,
                                 const int *__restrict__ cols, const double *__restrict__ sign,
-                                const int64_t *__restrict__ perm, double *__restrict__ out) {
+                                const int64_t *__restrict__ perm, double *__restrict__ out,
+                                int64_t row_base) {
   int64_t total = n * (int64_t)k;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = e / k;
     int j = (int)(e - r * k);
-    int64_t o = perm ? perm[r] : r;
+    int64_t o = perm ? perm[row_base + r] : row_base + r;
     out[o * k + j] = sign[j] * (double)S[r * ld + cols[j]];
   }
 }
@@ -840,8 +855,20 @@ struct Lobpcg {
   double anorm = 0, bmax = 0, ydenom = 0;
   int64_t zpos = 0;
   bool have_y = false;
+  // distributed mode: this rank owns global rows [row_base, row_base + n)
+  Comm *comm = nullptr;
+  const DistPart<T> *dp = nullptr;
+  int64_t n_global = 0, n_ext = 0;
+  DBuf<T> Xe, sendbuf;  // [local | halo] rows of the SpMM input; packed send rows
 
   Lobpcg(mg_ctx *c, const DevCSR<T> &a, const SolveSpec &s) : ctx(c), A(a), sp(s), n(a.n) {
+    if (s.comm && s.comm->nranks > 1) {
+      comm = s.comm;
+      dp = (const DistPart<T> *)s.dist;
+      require(dp != nullptr && dp->nloc == n, MG_ERR_INTERNAL, "distributed solve without a plan");
+    }
+    n_global = comm ? s.n_global : n;
+    n_ext = comm ? n + dp->nhalo : n;
     m = s.k;
     mp = (m + VN - 1) / VN * VN;
     ld = 3 * mp + VN;
@@ -910,7 +937,46 @@ struct Lobpcg {
       k_reduce_gram<<<grid_for(tot, 256, 4 * ctx->num_sms), 256, 0, ctx->stream>>>(
           a.g[q].part, grid_pass, g[q].rw, g[q].cw, g[q].sym, reds[q]);
       MG_CHECK_LAUNCH(ctx);
+      ar(reds[q], (size_t)tot);
     }
+  }
+
+  // sum (or max) a device fp64 array over ranks; no-op on one rank
+  void ar(double *p, size_t cnt, bool mx = false) {
+    if (comm) comm->allreduce(ctx, p, cnt, mx);
+  }
+
+  // fill the halo rows [n, n_ext) of a compact w-wide block whose local rows are set
+  void halo(T *X, int w) {
+    if (!comm) return;
+    if (dp->nsend > 0) {
+      k_pack_rows<T><<<grid_for(dp->nsend * w, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+          X, w, dp->send_rows.p, dp->nsend, sendbuf.p);
+      MG_CHECK_LAUNCH(ctx);
+    }
+    std::vector<int64_t> so(dp->soff), sc(dp->scnt), ro(dp->roff), rc(dp->rcnt);
+    for (size_t p = 0; p < so.size(); ++p) {
+      so[p] *= w;
+      sc[p] *= w;
+      ro[p] *= w;
+      rc[p] *= w;
+    }
+    comm->exchange(ctx, sendbuf.p, so.data(), sc.data(), X + (size_t)n * w, ro.data(), rc.data(),
+                   sizeof(T));
+  }
+
+  // dst = A * src[:, c0:c0+w]; in distributed mode the block is staged
+  // compactly and its halo rows are exchanged first
+  void spmm_into(const T *src, int lds, int c0, int w, T *dst, int ldd) {
+    if (!comm) {
+      spmm<T>(ctx, A, src + c0, lds, dst, ldd, w);
+      return;
+    }
+    k_copy_cols<T><<<grid_for(n * w, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        n, src, lds, c0, Xe.p, w, 0, w);
+    MG_CHECK_LAUNCH(ctx);
+    halo(Xe.p, w);
+    spmm<T>(ctx, A, Xe.p, w, dst, ldd, w);
   }
 
   GramSpec gspec(int r0, int rw, int c0, int cw, int sym, int use_as) {
@@ -920,7 +986,7 @@ struct Lobpcg {
   }
 
   void spmm_cols(int c0, int w) {
-    spmm<T>(ctx, A, S.p + c0, ld, AS.p + c0, ld, w);
+    spmm_into(S.p, ld, c0, w, AS.p + c0, ld);
     debug_check("spmm");
   }
 
@@ -960,6 +1026,7 @@ struct Lobpcg {
     MG_CHECK_LAUNCH(ctx);
     k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, nb, 2 * mp, colred.p);
     MG_CHECK_LAUNCH(ctx);
+    ar(colred.p, 2 * mp);
     out.resize(2 * mp);
     d2h_sync(ctx, out.data(), colred.p, 2 * mp * sizeof(double));
   }
@@ -974,6 +1041,7 @@ struct Lobpcg {
     MG_CHECK_LAUNCH(ctx);
     k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, nb, mp, theta.p);
     MG_CHECK_LAUNCH(ctx);
+    ar(theta.p, mp);
     th.resize(mp);
     d2h_sync(ctx, th.data(), theta.p, mp * sizeof(double));
   }
@@ -1070,12 +1138,12 @@ struct Lobpcg {
   }
 
   void place_normals(int c0, int w) {
-    int64_t need = n * (int64_t)w;
+    int64_t need = n_global * (int64_t)w;  // the stream covers every global row
     require(sp.normals != nullptr && zpos + need <= sp.n_normals, MG_ERR_INPUT,
             "standard-normal stream exhausted (need " + std::to_string(zpos + need) + ", have " +
                 std::to_string(sp.n_normals) + ")");
-    k_load_normals<T><<<grid_for(need, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-        n, w, sp.normals, zpos, sp.perm, S.p, ld, c0);
+    k_load_normals<T><<<grid_for(n * w, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        n, w, sp.normals, zpos, sp.perm, S.p, ld, c0, sp.row_base);
     MG_CHECK_LAUNCH(ctx);
     zpos += need;
   }
@@ -1096,7 +1164,7 @@ struct Lobpcg {
       // refill (eigensolver.py:188-193): extra = stream (n, m-nk), deflated, + A-images
       place_normals(nk, m - nk);
       deflate_cols(nk, m, 0, mp);
-      spmm<T>(ctx, A, S.p, ld, tmpblk.p, mp, mp);
+      spmm_into(S.p, ld, 0, mp, tmpblk.p, mp);
       k_copy_cols<T><<<grid_for(n * (m - nk), 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
           n, tmpblk.p, mp, nk, AS.p, ld, nk, m - nk);
       MG_CHECK_LAUNCH(ctx);
@@ -1121,6 +1189,7 @@ struct Lobpcg {
     MG_CHECK_LAUNCH(ctx);
     k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, nb, 2 * mp, colred.p);
     MG_CHECK_LAUNCH(ctx);
+    ar(colred.p, 2 * mp);
     MG_CUDA(cudaMemcpyAsync(colred.p + 2 * mp, theta.p, mp * sizeof(double),
                             cudaMemcpyDeviceToDevice, ctx->stream));
     MG_CUDA(cudaMemcpyAsync(colred.p + 3 * mp, status.p, 6 * sizeof(int), cudaMemcpyDeviceToDevice,
@@ -1246,6 +1315,8 @@ struct Lobpcg {
     k_reduce_gram2<<<grid_for(2 * w * w, 256, 4 * ctx->num_sms), 256, 0, ctx->stream>>>(
         gpart.p, grid_fast, w, Gr0.p, Gr1.p);
     MG_CHECK_LAUNCH(ctx);
+    ar(Gr0.p, (size_t)w * w);
+    ar(Gr1.p, (size_t)w * w);
     FastArgs fa{};
     fa.m = m;
     fa.mp = mp;
@@ -1307,6 +1378,7 @@ struct Lobpcg {
     }
     k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, grid_upd, 2 * mp, colred.p);
     MG_CHECK_LAUNCH(ctx);
+    ar(colred.p, 2 * mp);
     MG_CUDA(cudaMemcpyAsync(colred.p + 2 * mp, theta.p, mp * sizeof(double),
                             cudaMemcpyDeviceToDevice, ctx->stream));
     MG_CUDA(cudaMemcpyAsync(colred.p + 3 * mp, status.p, 6 * sizeof(int), cudaMemcpyDeviceToDevice,
@@ -1354,8 +1426,8 @@ struct Lobpcg {
   SolveResult run(double anorm_in, const double *b_dev, const double *diag_dev, double *eigvecs) {
     SolveResult res;
     require(m >= 1, MG_ERR_INPUT, "block size must be >= 1, got " + std::to_string(m));
-    require(m <= n, MG_ERR_INPUT,
-            "block size " + std::to_string(m) + " exceeds dimension " + std::to_string(n));
+    require(m <= n_global, MG_ERR_INPUT,
+            "block size " + std::to_string(m) + " exceeds dimension " + std::to_string(n_global));
     require(3 * mp + VN <= kMaxL, MG_ERR_INPUT, "block size too large for this build");
     anorm = anorm_in;
     int64_t ntiles = (n + kTR - 1) / kTR;
@@ -1367,8 +1439,12 @@ struct Lobpcg {
     bw.alloc(ctx, n);
     prec.alloc(ctx, n);
     tmpblk.alloc(ctx, n * mp);
-    Wc.alloc(ctx, n * mp);
+    Wc.alloc(ctx, n_ext * mp);
     Wc.zero();
+    if (comm) {
+      Xe.alloc(ctx, n_ext * 3 * mp);
+      sendbuf.alloc(ctx, std::max<int64_t>(dp->nsend, 1) * 3 * mp);
+    }
     int g = grid_for(n, 256, ctx->num_sms * 16);
     k_vec_T<T><<<g, 256, 0, ctx->stream>>>(n, b_dev, bw.p, 0);
     MG_CHECK_LAUNCH(ctx);
@@ -1391,6 +1467,12 @@ struct Lobpcg {
     MG_CUDA(cudaFuncSetAttribute(k_tile_pass<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smax_pass));
     bmax = max_f64_const(ctx, b_dev, n);
+    if (comm) {
+      DBuf<double> t(ctx, 1);
+      MG_CUDA(cudaMemcpyAsync(t.p, &bmax, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      ar(t.p, 1, true);
+      d2h_sync(ctx, &bmax, t.p, sizeof(double));
+    }
     have_y = sp.deflate != nullptr;
     if (have_y) {  // deflation vector y at column 3mp, and y'By
       k_set_col<T><<<g, 256, 0, ctx->stream>>>(n, sp.deflate, 0.0, S.p, ld, 3 * mp);
@@ -1453,6 +1535,7 @@ struct Lobpcg {
         // with one wide SpMM at every full re-orthonormalisation
         spmm_cols(0, 3 * mp);
       } else {
+        halo(Wc.p, mp);
         spmm<T>(ctx, A, Wc.p, mp, AS.p + 2 * mp, ld, mp);  // compact W: L2-resident gathers
         debug_check("spmm");
       }
@@ -1532,14 +1615,14 @@ struct Lobpcg {
     DBuf<double> pv(ctx, (size_t)nb * mp), pval(ctx, (size_t)nb * mp);
     DBuf<int64_t> pi(ctx, (size_t)nb * mp);
     k_colamax<T><<<nb, R * mp, (size_t)R * mp * 3 * sizeof(double), ctx->stream>>>(
-        n, S.p, ld, mp, sp.perm, pv.p, pi.p, pval.p);
+        n, S.p, ld, mp, sp.perm, pv.p, pi.p, pval.p, sp.row_base);
     MG_CHECK_LAUNCH(ctx);
     std::vector<double> hv((size_t)nb * mp), hval((size_t)nb * mp);
     std::vector<int64_t> hi((size_t)nb * mp);
     d2h_sync(ctx, hv.data(), pv.p, hv.size() * sizeof(double));
     d2h_sync(ctx, hval.data(), pval.p, hval.size() * sizeof(double));
     d2h_sync(ctx, hi.data(), pi.p, hi.size() * sizeof(int64_t));
-    std::vector<double> sign(m);
+    std::vector<double> sign(m), gbest;
     std::vector<int> cols(m);
     for (int j = 0; j < m; ++j) {
       int c = order[j];
@@ -1556,6 +1639,33 @@ struct Lobpcg {
       }
       sign[j] = val < 0.0 ? -1.0 : 1.0;
       cols[j] = c;
+      if (comm) {  // best over ranks: slots [best, index, value] per rank
+        gbest.push_back(best);
+        gbest.push_back((double)bi);
+        gbest.push_back(val);
+      }
+    }
+    if (comm) {
+      const int R = comm->nranks;
+      DBuf<double> slots(ctx, (size_t)R * m * 3);
+      slots.zero();
+      MG_CUDA(cudaMemcpyAsync(slots.p + (size_t)comm->rank * m * 3, gbest.data(),
+                              gbest.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      ar(slots.p, (size_t)R * m * 3);
+      std::vector<double> hs((size_t)R * m * 3);
+      d2h_sync(ctx, hs.data(), slots.p, hs.size() * sizeof(double));
+      for (int j = 0; j < m; ++j) {
+        double best = -1.0, val = 0.0, bi = 1e300;
+        for (int p = 0; p < R; ++p) {
+          const double *e = &hs[((size_t)p * m + j) * 3];
+          if (e[0] > best || (e[0] == best && e[1] < bi)) {
+            best = e[0];
+            bi = e[1];
+            val = e[2];
+          }
+        }
+        sign[j] = val < 0.0 ? -1.0 : 1.0;
+      }
     }
     DBuf<double> dsign(ctx, m);
     DBuf<int> dcols(ctx, m);
@@ -1563,9 +1673,12 @@ struct Lobpcg {
                             ctx->stream));
     MG_CUDA(cudaMemcpyAsync(dcols.p, cols.data(), m * sizeof(int), cudaMemcpyHostToDevice,
                             ctx->stream));
+    if (comm)  // every rank writes its rows of the full block; the sum gathers it
+      MG_CUDA(cudaMemsetAsync(eigvecs, 0, (size_t)n_global * m * sizeof(double), ctx->stream));
     k_write_vectors<T><<<grid_for(n * m, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-        n, S.p, ld, m, dcols.p, dsign.p, sp.perm, eigvecs);
+        n, S.p, ld, m, dcols.p, dsign.p, sp.perm, eigvecs, sp.row_base);
     MG_CHECK_LAUNCH(ctx);
+    ar(eigvecs, (size_t)n_global * m);
     sync(ctx);
     res.normals_used = zpos;
     res.fast_steps = fast_steps;

@@ -1,0 +1,85 @@
+"""Row-partitioned solve on one B200: R virtual ranks as threads
+with the host-rendezvous communicator, compared with the single-GPU embed.
+
+The setup is replicated, so Q and the nnz counts are identical; eps and the
+eigenpairs come from iterative solves whose reductions are summed in a
+different order (per-rank partials, then the allreduce), so they agree to the
+solver tolerance, like the reordered single-GPU run (test_gpu_configs), and
+mu / A / b inherit eps's last-ulp noise.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import principal_angles
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mg():
+    import paper_2112_07862_b200 as mg
+    return mg
+
+
+def _single(g, K, cfg):
+    from paper_2112_07862_b200 import core
+    n, ptr, idx, w = g
+    res, b, dg = core.embed_arrays(n, ptr, idx, w, K, cfg)
+    return res, b.cpu().numpy(), dg
+
+
+def _dist(g, K, cfg, R, reorder=True):
+    from paper_2112_07862_b200 import dist
+    n, ptr, idx, w = g
+    return dist.run_local(R, lambda comm, ctx, r: dist.embed_arrays_dist(
+        comm, ctx, 0, n, ptr, idx, w, K, cfg, reorder=reorder))
+
+
+def _compare(g, K, cfg, R, ev_tol, ang_tol):
+    res0, b0, dg0 = _single(g, K, cfg)
+    f64 = cfg.precision == "fp64"
+    rt = 1e-9 if f64 else 1e-6  # eps / mu / b: inherited from the eps solve
+    outs = _dist(g, K, cfg, R)
+    assert len(outs) == R
+    for r, (res, b, dg) in enumerate(outs):
+        assert res.converged.all(), r
+        # replicated setup; b inherits eps's reduction-order noise (ulps)
+        np.testing.assert_allclose(b, b0, rtol=rt, atol=0)
+        assert dg.mu == pytest.approx(dg0.mu, rel=rt)
+        assert dg.epsilon == pytest.approx(dg0.epsilon, rel=rt)
+        assert dg.q_nnz == dg0.q_nnz and dg.a_nnz == dg0.a_nnz
+        ev = res.eigenvalues
+        assert np.max(np.abs(ev - res0.eigenvalues) / np.abs(res0.eigenvalues)) < ev_tol
+        vecs = res.eigenvectors
+        ang = principal_angles(vecs, res0.eigenvectors.cpu().numpy(), b)
+        assert ang.max() < ang_tol, ang
+        gram = vecs.T @ (b[:, None] * vecs)
+        assert np.max(np.abs(gram - np.eye(K + 1))) < (1e-8 if cfg.precision == "fp64" else 1e-4)
+    # every rank returns the same full embedding
+    for res, b, dg in outs[1:]:
+        np.testing.assert_array_equal(res.eigenvalues, outs[0][0].eigenvalues)
+        np.testing.assert_array_equal(res.eigenvectors, outs[0][0].eigenvectors)
+
+
+@pytest.mark.parametrize("R", [2, 3])
+def test_dist_small_natural_order(mg, R):
+    """n <= 4096: no reordering, large halos (every rank talks to every rank)."""
+    from paper_2112_07862_b200 import synthetic
+    g = synthetic.random_connected(np.random.default_rng(5), 1500, extra=3000, weighted=True)
+    cfg = mg.SolverConfig(k=5, tol=1e-8, max_iter=2000, seed=42)
+    _compare(g, 4, cfg, R, 1e-9, 1e-5)
+
+
+@pytest.mark.parametrize("R,precision", [(2, "fp64"), (4, "fp64"), (2, "fp32")])
+def test_dist_c2(mg, R, precision):
+    """Config 2 graph (100k kNN, Cuthill-McKee order, thin halos)."""
+    from paper_2112_07862_b200 import synthetic
+    g = synthetic.config_graph("c2")
+    cfg = mg.SolverConfig(k=5, tol=1e-6, max_iter=3000, seed=42, precision=precision)
+    if precision == "fp64":
+        _compare(g, 4, cfg, R, 1e-6, 3e-4)
+    else:
+        _compare(g, 4, cfg, R, 1e-4, 1e-2)
