@@ -8,9 +8,10 @@ and once more through the public API with host buffers (``e2e``).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--n N]
     python bench.py --impl reference ...   # CPU oracle port of the reference path
 
-Multi-GPU (torchrun, one rank per GPU): the path has no sharded
-implementation yet, so N GPUs run N independent replicas ("replicas only",
-DESIGN.md); value = mean per-embedding wall time, max over ranks.
+Multi-GPU (torchrun, one rank per GPU): ONE embed of the config graph with
+the LOBPCG solve row-partitioned over the N GPUs (setup replicated, NCCL halo
+exchange + Gram allreduce; dist.py / DESIGN.md 8(e)) -- strong scaling;
+value = per-embedding wall time, max over ranks.
 """
 
 from __future__ import annotations
@@ -175,7 +176,7 @@ def run_reference(args, cfg, n_full):
     cores = blas_threads()
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "n": n_full, "K": cfg.k, "tol": cfg.tol,
                        "precision": "fp64 (reference)"},
@@ -215,19 +216,16 @@ def main():
 
     world, rank, local = dist_setup()
     device = local if world > 1 else 0
-    if world > 1:
-        # one GPU per rank: the library context always uses device 0 of its process
-        os.environ["CUDA_VISIBLE_DEVICES"] = str(local)
     import torch
+    torch.cuda.set_device(device)
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(0)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
-    else:
-        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", device))
 
     import paper_2112_07862_b200 as mg
     from paper_2112_07862_b200 import _native as N, core
+    from paper_2112_07862_b200 import dist as mgdist
+    comm = mgdist.nccl_comm(rank, world, device) if world > 1 else None
 
     prec = args.precision or cfg.precision
     max_iter = args.max_iter or cfg.max_iter
@@ -239,16 +237,27 @@ def main():
     scfg = mg.SolverConfig(k=K + 1, tol=cfg.tol, max_iter=max_iter, seed=42, precision=prec)
     G = mg.Graph(n, ptr, idx, w)
     zcount = core._stream_size(n, max(K + 1, 8))
-    z, _ = core._normals(42, zcount)
-    dev_inputs = (*G._device(), z)
-    ext = torch.cuda.ExternalStream(N.stream_handle(0))
+    zh = np.random.default_rng(42).standard_normal(zcount)
+    dd = torch.device("cuda", device)
+    dev_inputs = (torch.from_numpy(np.ascontiguousarray(ptr, np.int64)).to(dd),
+                  torch.from_numpy(np.ascontiguousarray(idx, np.int64)).to(dd),
+                  torch.from_numpy(np.ascontiguousarray(w, np.float64)).to(dd),
+                  torch.from_numpy(zh).to(dd))
+    del zh
+    ext = torch.cuda.ExternalStream(N.stream_handle(device), device=dd)
+
+    def embed_dev():
+        if comm is None:
+            return core.embed_arrays(n, None, None, None, K, scfg, device_inputs=dev_inputs)
+        return mgdist.embed_arrays_dist(comm, N.context(device), device, n, None, None, None, K,
+                                        scfg, device_inputs=dev_inputs)
 
     def one_step():
         start = torch.cuda.Event(enable_timing=True)
         stop = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         start.record(ext)
-        res, b, dg = core.embed_arrays(n, None, None, None, K, scfg, device_inputs=dev_inputs)
+        res, b, dg = embed_dev()
         stop.record(ext)
         stop.synchronize()
         return start.elapsed_time(stop) / 1e3, res, dg
@@ -258,9 +267,9 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    N.set_profiling(True)
-    N.stats()  # clear
-    l0 = N.launch_count()
+    N.set_profiling(True, device)
+    N.stats(device)  # clear
+    l0 = N.launch_count(device)
     times, last = [], None
     with ClockSampler(device) as clk:
         for _ in range(args.steps):
@@ -268,12 +277,12 @@ def main():
             times.append(dt)
             last = (res, dg)
     torch.cuda.synchronize()
-    launches = N.launch_count() - l0
-    st = N.stats()
-    N.set_profiling(False)
+    launches = N.launch_count(device) - l0
+    st = N.stats(device)
+    N.set_profiling(False, device)
     t_local = float(np.mean(times))
     if world > 1:
-        tt = torch.tensor([t_local], device="cuda")
+        tt = torch.tensor([t_local], device=dd)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_max = float(tt.item())
     else:
@@ -285,17 +294,27 @@ def main():
     for _ in range(max(1, min(args.steps, 2))):
         Gh = mg.Graph(n, ptr, idx, w)
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
-        emb = mg.embed(Gh, K, scfg, require_convergence=False)
+        if comm is None:
+            mg.embed(Gh, K, scfg, require_convergence=False)
+        else:
+            mgdist.embed_dist(comm, Gh, K, scfg, device=device, require_convergence=False)
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
+    if world > 1:  # job time = slowest rank
+        te = torch.tensor([float(np.mean(e2e_times))], device=dd)
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        e2e_times = [float(te.item())]
     e2e = float(np.mean(e2e_times))
     h2d = 8 * (n + 1) + 16 * int(idx.size) + 8 * zcount
     d2h = 8 * n * K + 8 * n
 
     if rank != 0:
-        if world > 1:
-            torch.distributed.destroy_process_group()
+        if comm is not None:
+            comm.close()
+        torch.distributed.destroy_process_group()
         return
     hbm, bf16, peak_src = load_peaks()
     sp = st["spmm"]
@@ -309,12 +328,13 @@ def main():
     line = {
         "metric": METRIC, "value": t_max, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max * 1e3, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None,
+        "scaling": "strong", "vs_baseline": None,
         "dtype": "f32" if prec == "fp32" else "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "description": cfg.description, "n": n,
                    "graph_nnz": int(idx.size), "K": K, "block": K + 1, "tol": cfg.tol,
                    "max_iter": max_iter, "precision": prec,
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": f"rows{world} (1-D row partition, NCCL halo + Gram allreduce)"
+                   if world > 1 else "single",
                    "l2": "inputs larger than L2 (126 MB)" if n >= 1_000_000 else "L2-resident",
                    "iterations": int(res.iterations), "eps_iterations": int(dg.eps_iterations),
                    "A_nnz": int(dg.a_nnz), "Q_nnz": int(dg.q_nnz),
@@ -351,6 +371,8 @@ def main():
                       f"linearly to N={n} and the {int(res.iterations)} iterations the GPU needed",
             "detail": detail}
     print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 

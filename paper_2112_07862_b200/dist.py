@@ -115,9 +115,11 @@ def plan(indptr, indices, nranks: int, rank: int) -> dict:
 
 def embed_arrays_dist(comm: Comm, ctx, device: int, n, indptr, indices, weights, k: int,
                       cfg: SolverConfig | None = None, literal_diagonal=False,
-                      check_connected=True, reorder=True):
+                      check_connected=True, reorder=True, device_inputs=None):
     """Distributed ``core.embed_arrays``: every rank passes the full graph (host
-    arrays) and receives the full K+1 eigenpairs, b and diagnostics."""
+    arrays, or ``device_inputs`` = (indptr, indices, weights, normals) CUDA
+    tensors on ``device``) and receives the full K+1 eigenpairs, b and
+    diagnostics (eigenvectors stay on the device)."""
     import torch
     dev = torch.device("cuda", device)
     cfg = cfg or SolverConfig(k=k + 1)
@@ -125,11 +127,15 @@ def embed_arrays_dist(comm: Comm, ctx, device: int, n, indptr, indices, weights,
     s.reserved = 1
     s.reorder = 1 if reorder else 0
     m = k + 1
-    p = torch.from_numpy(np.ascontiguousarray(indptr, dtype=np.int64)).to(dev)
-    i = torch.from_numpy(np.ascontiguousarray(indices, dtype=np.int64)).to(dev)
-    w = torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float64)).to(dev)
-    nz = _core._stream_size(n, max(m, min(8, max(n - 1, 1))))
-    z = torch.from_numpy(np.random.default_rng(cfg.seed).standard_normal(nz)).to(dev)
+    if device_inputs is None:
+        p = torch.from_numpy(np.ascontiguousarray(indptr, dtype=np.int64)).to(dev)
+        i = torch.from_numpy(np.ascontiguousarray(indices, dtype=np.int64)).to(dev)
+        w = torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float64)).to(dev)
+        nz = _core._stream_size(n, max(m, min(8, max(n - 1, 1))))
+        z = torch.from_numpy(np.random.default_rng(cfg.seed).standard_normal(nz)).to(dev)
+    else:
+        p, i, w, z = device_inputs
+        nz = int(z.numel())
     P = torch.empty(max(n * m, 1), dtype=torch.float64, device=dev)
     b = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
     ev, rn = np.zeros(m), np.zeros(m)
@@ -150,10 +156,10 @@ def embed_arrays_dist(comm: Comm, ctx, device: int, n, indptr, indices, weights,
                C.c_void_p(P.data_ptr()), C.c_void_p(b.data_ptr()), C.byref(out), C.byref(dg))
     except N.NativeError as e:
         _core._raise_native(e)
-    res = EigenResult(eigenvalues=ev.copy(), eigenvectors=P[:n * m].view(n, m).cpu().numpy(),
+    res = EigenResult(eigenvalues=ev.copy(), eigenvectors=P[:n * m].view(n, m),
                       iterations=int(out.iterations), residual_norms=rn.copy(),
                       converged=cv.astype(bool), ritz_sum_history=list(hist[:out.history_len]))
-    return res, b[:n].cpu().numpy(), dg
+    return res, b[:n], dg
 
 
 def embed_dist(comm: Comm, g, k: int, cfg: SolverConfig | None = None, device: int = 0,
@@ -165,6 +171,8 @@ def embed_dist(comm: Comm, g, k: int, cfg: SolverConfig | None = None, device: i
     ctx = ctx if ctx is not None else N.context(device)
     res, b, dg = embed_arrays_dist(comm, ctx, device, g.n, g.indptr, g.indices, g.weights, k,
                                    cfg, literal_diagonal)
+    res.eigenvectors = res.eigenvectors.cpu().numpy()
+    b = b.cpu().numpy()
     if require_convergence:
         _core.require_converged(res, "embedding eigensolve")
     return Embedding(P=res.eigenvectors[:, 1:], method="proposed",

@@ -34,8 +34,11 @@ def _single(g, K, cfg):
 def _dist(g, K, cfg, R, reorder=True):
     from paper_2112_07862_b200 import dist
     n, ptr, idx, w = g
-    return dist.run_local(R, lambda comm, ctx, r: dist.embed_arrays_dist(
-        comm, ctx, 0, n, ptr, idx, w, K, cfg, reorder=reorder))
+    def body(comm, ctx, r):
+        res, b, dg = dist.embed_arrays_dist(comm, ctx, 0, n, ptr, idx, w, K, cfg, reorder=reorder)
+        res.eigenvectors = res.eigenvectors.cpu().numpy()
+        return res, b.cpu().numpy(), dg
+    return dist.run_local(R, body)
 
 
 def _compare(g, K, cfg, R, ev_tol, ang_tol):
@@ -83,3 +86,25 @@ def test_dist_c2(mg, R, precision):
         _compare(g, 4, cfg, R, 1e-6, 3e-4)
     else:
         _compare(g, 4, cfg, R, 1e-4, 1e-2)
+
+
+def test_nccl_single_rank_communicator(mg):
+    """NCCL is loaded (dlopen), a unique id is made and a 1-rank communicator
+    runs the distributed entry point (which then takes the unpartitioned path)."""
+    from paper_2112_07862_b200 import _native as N, dist
+    import ctypes as C
+    uid = dist.nccl_unique_id()
+    assert len(uid) == 128 and any(uid)
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    h = C.c_void_p()
+    N.call("mg_comm_create_nccl", N.context(0), 1, 0, C.cast(buf, C.c_void_p), C.byref(h))
+    comm = dist.Comm(h, 0, 1, "nccl")
+    from paper_2112_07862_b200 import synthetic
+    g = mg.Graph(*synthetic.random_connected(np.random.default_rng(2), 600, extra=900,
+                                             weighted=True))
+    cfg = mg.SolverConfig(k=4, tol=1e-8, max_iter=2000, seed=42)
+    e1 = dist.embed_dist(comm, g, 3, cfg)
+    e0 = mg.embed(g, 3, cfg)
+    np.testing.assert_array_equal(e1.eigenvalues, e0.eigenvalues)
+    np.testing.assert_array_equal(e1.P, e0.P)
+    comm.close()
