@@ -210,6 +210,16 @@ int mg_embed_host(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *
                   int32_t check_connected, const double *normals, int64_t n_normals,
                   double *P, double *b, mg_solver_out *out, mg_embed_diag *diag);
 
+/* Gram pair of the fp32 solve on the tensor cores (tcgen05, 3xTF32):
+ * GB = S' diag(b) S, GA = S' AS over the first w columns of row-major n x ld
+ * fp32 blocks (64 < w <= 128, ld % 4 == 0); outputs w x w row-major fp64.
+ * Replaces, in one pass over the block, the B-inner products of the
+ * reference's _b_mgs_pair (eigensolver.py:127, 143, 145: prefix.T @ (b*rest),
+ * U.T @ (b*v), v @ (b*v)) and the Rayleigh-Ritz Gram S.T @ AS
+ * (eigensolver.py:251), at the K = 16..32 block widths. */
+int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float *S,
+                     const float *AS, const float *b, double *GB, double *GA);
+
 /* ---------------------------------------------------- multi-GPU (8(e)) ---
  * 1-D row partition of the solve over ranks (one process per GPU).  The
  * setup (Q, eps, mu, A, b) is replicated; each LOBPCG SpMM exchanges halo

@@ -80,6 +80,7 @@ SIGNATURES = {
                  C.POINTER(SolverOut), C.POINTER(EmbedDiag)],
     "mg_embed_host": [vp, i64, vp, vp, vp, i32, C.POINTER(SolverCfg), i32, i32, i32, vp, i64,
                       vp, vp, C.POINTER(SolverOut), C.POINTER(EmbedDiag)],
+    "mg_gram_pair_f32": [vp, i64, i32, i32, vp, vp, vp, vp, vp],
     # multi-GPU (row-partitioned solve)
     "mg_nccl_unique_id": [vp],
     "mg_comm_create_nccl": [vp, i32, i32, vp, C.POINTER(vp)],

@@ -8,6 +8,7 @@
 #include "mg_block.cuh"
 #include "mg_comm.cuh"
 #include "mg_dist.cuh"
+#include "mg_tc.cuh"
 #include "mg_graph.cuh"
 #include "mg_small.cuh"
 
@@ -698,6 +699,18 @@ int mg_embed(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indic
   require(cfg != nullptr, MG_ERR_INPUT, "cfg is NULL");
   return embed_impl(ctx, n, indptr, indices, weights, K, cfg, literal_diagonal,
                     require_convergence, check_connected, normals, n_normals, P, b, out, diag);
+  MG_API_END
+}
+
+int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float *S,
+                     const float *AS, const float *b, double *GB, double *GA) {
+  MG_API_BEGIN(ctx)
+  require(n >= 1 && w >= 1 && ld >= w, MG_ERR_INPUT, "bad Gram shape");
+  require(gram_tc_supported(w), MG_ERR_INPUT,
+          "tensor-core Gram pair needs 64 < w <= 128 (set MG_TC=1)");
+  DBuf<double> part;
+  gram_pair_tc(ctx, n, ld, w, S, AS, b, GB, GA, part);
+  sync(ctx);
   MG_API_END
 }
 

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
 }
 
 // sum CTA partials (fixed order) and mirror the symmetric lower blocks
-__global__ void k_reduce_gram2(const double *__restrict__ part, int nb_cta, int w,
+static __global__ void k_reduce_gram2(const double *__restrict__ part, int nb_cta, int w,
                                double *__restrict__ GB, double *__restrict__ GA) {
   const int tot = 2 * w * w;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {

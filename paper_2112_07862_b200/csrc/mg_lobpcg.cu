@@ -29,6 +29,7 @@
 #include "mg_fastk.cuh"
 #include "mg_eig.cuh"
 #include "mg_dist.cuh"
+#include "mg_tc.cuh"
 
 namespace mg {
 
@@ -1211,7 +1212,8 @@ struct Lobpcg {
   int grid_fast = 0, grid_upd = 0;
   size_t gram2_smem = 0, upd_smem = 0, fast_smem = 0;
   int fast_global = 0;
-  DBuf<double> gpart;
+  DBuf<double> gpart, tcpart;
+  bool use_tc = false;  // fp32 wide blocks: tcgen05 3xTF32 Gram pair (mg_tc.cuh)
   int64_t fast_steps = 0, fast_fallbacks = 0;
 
   int tk_gram = 32, ns_gram = 3, tk_upd = 32, rt_upd = 8;
@@ -1284,6 +1286,7 @@ struct Lobpcg {
     grid_upd = (int)std::min<int64_t>((n + tk_upd - 1) / tk_upd, ctx->num_sms);
     const int w = 3 * mp;
     gpart.alloc(ctx, (size_t)grid_fast * 2 * w * w);
+    use_tc = sizeof(T) == 4 && gram_tc_supported(w);
     fast_ok = true;
   }
 
@@ -1300,6 +1303,13 @@ struct Lobpcg {
     ga.nsym = ga.nb * (ga.nb + 1) / 2;
     ga.part = gpart.p;
     const int total = 2 * ga.nsym;
+    if constexpr (sizeof(T) == 4) {
+      if (use_tc) {
+        gram_pair_tc(ctx, n, ld, w, (const float *)S.p, (const float *)AS.p,
+                     (const float *)bw.p, Gr0.p, Gr1.p, tcpart);
+        goto gram_done;
+      }
+    }
     {
       ProfScope ps(ctx, PROF_GRAM, 2.0 * n * ld * sizeof(T));
       for (int lo = 0; lo < total; lo += kFThreads) {
@@ -1315,6 +1325,7 @@ struct Lobpcg {
     k_reduce_gram2<<<grid_for(2 * w * w, 256, 4 * ctx->num_sms), 256, 0, ctx->stream>>>(
         gpart.p, grid_fast, w, Gr0.p, Gr1.p);
     MG_CHECK_LAUNCH(ctx);
+  gram_done:
     ar(Gr0.p, (size_t)w * w);
     ar(Gr1.p, (size_t)w * w);
     FastArgs fa{};
