@@ -7,7 +7,6 @@ namespace mg {
 static constexpr int kTcThreads = 320;  // 10 warps: producer, MMA, 8 workers
 static constexpr int kTcM = 128;        // Gram rows (S columns), zero-padded
 static constexpr int kTcN = 64;         // Gram columns per CTA (half), zero-padded
-static constexpr int kTcMaxItems = 4;   // conversion items per worker thread and tile
 static constexpr int kTcFold = 32;      // TMEM groups (64 rows each) per fp64 fold
 
 // ------------------------------------------------------------ tcgen05 PTX ---
@@ -125,10 +124,11 @@ __device__ __forceinline__ void split_tf32(float x, float (&p)[3]) {
 // outstanding bulk copies per SM to cover HBM latency), OS operand stages.
 template <int NS>
 struct TcCfg {
-  static constexpr int TK = 16;
-  static constexpr int FL = 4;
-  static constexpr int RS = 8;
-  static constexpr int OS = NS == 3 ? 2 : 3;
+  static constexpr int TK = NS == 3 ? 16 : 32;
+  static constexpr int FL = NS == 3 ? 4 : 2;
+  static constexpr int RS = NS == 3 ? 8 : 3;
+  static constexpr int OS = NS == 3 ? 2 : 2;
+  static constexpr int MI = (112 + 2 * 56) * (TK / 4) / (kTcThreads - 64) + 1;  // items/thread
   static constexpr int NPROD = NS == 3 ? 6 : 3;
   __host__ __device__ static constexpr int pa(int t) { return t == 1 ? 1 : t == 3 ? 2 : t == 5 ? 1 : 0; }
   __host__ __device__ static constexpr int pb(int t) { return t == 2 ? 1 : t == 4 ? 2 : t == 5 ? 1 : 0; }
@@ -323,9 +323,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // my_src: byte offset of (row 4kg, column) in the raw stage | kg << 24;
     // my_dst: byte offset in the operand stage | bit 28 (B piece) | bit 31 (scale by b)
     const int nA = w * (TK / 4), nB = ncol * (TK / 4);
-    int my_src[kTcMaxItems], my_dst[kTcMaxItems], my_n = 0;
+    int my_src[C::MI], my_dst[C::MI], my_n = 0;
 #pragma unroll
-    for (int u = 0; u < kTcMaxItems; ++u) {
+    for (int u = 0; u < C::MI; ++u) {
       const int it = wt + u * NW;
       my_src[u] = my_dst[u] = 0;
       if (it < nA + 2 * nB) {
@@ -375,9 +375,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       const char *rbase = reinterpret_cast<const char *>(rS);
       char *obase = reinterpret_cast<char *>(op0 + (size_t)so * OP);
-      float xs[kTcMaxItems][4];
+      float xs[C::MI][4];
 #pragma unroll
-      for (int u = 0; u < kTcMaxItems; ++u) {  // all loads first (independent)
+      for (int u = 0; u < C::MI; ++u) {  // all loads first (independent)
         if (u < my_n) {
           const float *src = reinterpret_cast<const float *>(rbase + (my_src[u] & 0xFFFFFF));
           const bool sb = my_dst[u] < 0;
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&raw_empty[s]);  // raw stage s no longer read
 #pragma unroll
-      for (int u = 0; u < kTcMaxItems; ++u) {
+      for (int u = 0; u < C::MI; ++u) {
         if (u < my_n) {
           float pc[4][3];
 #pragma unroll
