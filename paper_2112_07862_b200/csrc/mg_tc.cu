@@ -466,6 +466,326 @@ __global__ void k_reduce_gram_tc(const double *__restrict__ part, int npairs, in
   }
 }
 
+// ------------------------------------------------------ update (tcgen05) ---
+// P = S Zp, X = S Zx (Zx = Zp + [Yx; 0; 0]) and the same for AS, as one
+// tensor-core GEMM per matrix: D[128 rows x 80] = S[rows, 0:K] * [Zp | Zx]
+// with 3xTF32 pieces; then the residual block W = prec (AX - b X theta), its
+// column norms, and the write-back of [X P W] / [AX AP] / Wc.
+//   A operand: S / AS row tiles (K-major, converted from row-major float4
+//   loads, 32 K per stage); B operand: [Zp | Zx] pieces resident in smem.
+static constexpr int kUpM = 128;      // rows per tile (MMA M)
+static constexpr int kUpN = 80;       // [P | X] columns (2 * mp <= 80), zero-padded
+static constexpr int kUpKC = 32;      // K per stage
+static constexpr int kUpKmax = 112;   // w <= 112
+static constexpr int kUpThreads = 256;
+
+struct UpdTcArgs {
+  int64_t n;
+  int ld, w, m, mp;
+  const int *skip;   // device flag: nonzero -> return (fallback iteration)
+  double *part;      // [grid][2*mp] column partials (rn^2, x^2)
+  float *wc;         // compact W (n x mp)
+};
+
+__host__ __device__ constexpr size_t up_b_piece() { return (size_t)kUpN * kUpKmax * 4; }
+__host__ __device__ constexpr size_t up_a_piece() { return (size_t)kUpM * kUpKC * 4; }
+__host__ __device__ constexpr size_t up_smem() {
+  return 2 * up_b_piece() + 2 * 4 * up_a_piece() + 64 * 4 + 16 * 8 + 16;
+}
+
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, float *v) {
+  uint32_t r0, r1;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  v[0] = __uint_as_float(r0);
+  v[1] = __uint_as_float(r1);
+}
+
+__global__ void __launch_bounds__(kUpThreads, 1)
+    k_update_tc(float *__restrict__ S, float *__restrict__ AS, const float *__restrict__ b,
+                const float *__restrict__ prec, const float *__restrict__ Mg,
+                const double *__restrict__ theta, UpdTcArgs a) {
+  if (*a.skip) return;
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char *zb = sm;                          // [Zp|Zx] hi, lo (K-major, N=80 x K=112)
+  unsigned char *st0 = sm + 2 * up_b_piece();      // 2 stages x [S hi, S lo, AS hi, AS lo]
+  float *sth = reinterpret_cast<float *>(st0 + 2 * 4 * up_a_piece());  // theta (mp <= 40)
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sth + 64);
+  uint64_t *st_empty = bars, *tm_full = bars + 2, *tm_empty = bars + 4;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 8);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ld = a.ld, w = a.w, mp = a.mp, m = a.m;
+  constexpr uint32_t LBO_A = (kUpM / 8) * 128, LBO_B = (kUpN / 8) * 128, SBO = 128;
+
+  // B operand: element (n, k) at (n/8)*128 + (n%8)*16 + (k/4)*LBO_B + (k%4)*4
+  //   n < mp: Zp[k][n];  mp <= n < 2mp: Zx[k][n-mp] = Zp[k][n-mp] + (k < mp ? Yx[k][n-mp] : 0)
+  for (int e = tid; e < kUpN * kUpKmax; e += kUpThreads) {
+    const int n = e % kUpN, k = e / kUpN;
+    float v = 0.f;
+    if (k < w) {
+      if (n < mp) v = Mg[k * mp + n];
+      else if (n < 2 * mp) {
+        const int c = n - mp;
+        v = Mg[k * mp + c] + (k < mp ? Mg[w * mp + k * mp + c] : 0.f);
+      }
+    }
+    float p[3];
+    split_tf32<2>(v, p);
+    const int off = ((n >> 3) * 128 + (n & 7) * 16 + (k >> 2) * LBO_B + (k & 3) * 4) >> 2;
+    reinterpret_cast<float *>(zb)[off] = p[0];
+    reinterpret_cast<float *>(zb + up_b_piece())[off] = p[1];
+  }
+  for (int e = tid; e < 64; e += kUpThreads) sth[e] = e < m ? (float)theta[e] : 0.f;
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&st_empty[s], 1);
+      mbar_init(&tm_full[s], 1);
+      mbar_init(&tm_empty[s], kUpThreads / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_proxy_async();
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  const int64_t ntiles = (a.n + kUpM - 1) / kUpM;
+  const int64_t t_begin = ntiles * blockIdx.x / gridDim.x;
+  const int64_t t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
+  const int T = (int)(t_end - t_begin);
+  const int nkc = (w + kUpKC - 1) / kUpKC;  // K stages per tile
+  // conversion mapping: lane -> (row r8 = lane % 8 within an 8-row group,
+  // 16-byte K chunk c4 = lane / 8 + 4 * half); a warp loads 8 rows x 64 B
+  const int q = warp & 3, half = warp >> 2;
+  float sr[18], sx[18];
+#pragma unroll
+  for (int j = 0; j < 18; ++j) sr[j] = sx[j] = 0.f;
+
+  float4 ld_s[4], ld_a[4];  // this thread's share of one K stage (S and AS)
+  // item j (0..3): row = warp * 16 + (j >> 1) * 8 + lane % 8 ... covering 128 rows
+  auto load_stage = [&](int64_t row0, int kc) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = warp * 16 + (j >> 1) * 8 + (lane & 7);
+      const int c4 = (lane >> 3) + 4 * (j & 1);  // 0..7
+      const int col = kc * kUpKC + c4 * 4;
+      const int64_t row = row0 + r;
+      float4 vs = make_float4(0.f, 0.f, 0.f, 0.f), va = vs;
+      if (row < a.n && col < ld) {
+        vs = __ldg(reinterpret_cast<const float4 *>(S + row * ld + col));
+        va = __ldg(reinterpret_cast<const float4 *>(AS + row * ld + col));
+      }
+      ld_s[j] = vs;
+      ld_a[j] = va;
+    }
+  };
+  auto store_stage = [&](int st) {
+    unsigned char *base = st0 + (size_t)st * 4 * up_a_piece();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = warp * 16 + (j >> 1) * 8 + (lane & 7);
+      const int c4 = (lane >> 3) + 4 * (j & 1);
+      const int off = (r >> 3) * 128 + (r & 7) * 16 + c4 * LBO_A;
+      float ps[4][3], pa[4][3];
+      split_tf32<2>(ld_s[j].x, ps[0]);
+      split_tf32<2>(ld_s[j].y, ps[1]);
+      split_tf32<2>(ld_s[j].z, ps[2]);
+      split_tf32<2>(ld_s[j].w, ps[3]);
+      split_tf32<2>(ld_a[j].x, pa[0]);
+      split_tf32<2>(ld_a[j].y, pa[1]);
+      split_tf32<2>(ld_a[j].z, pa[2]);
+      split_tf32<2>(ld_a[j].w, pa[3]);
+      *reinterpret_cast<float4 *>(base + off) = make_float4(ps[0][0], ps[1][0], ps[2][0], ps[3][0]);
+      *reinterpret_cast<float4 *>(base + up_a_piece() + off) =
+          make_float4(ps[0][1], ps[1][1], ps[2][1], ps[3][1]);
+      *reinterpret_cast<float4 *>(base + 2 * up_a_piece() + off) =
+          make_float4(pa[0][0], pa[1][0], pa[2][0], pa[3][0]);
+      *reinterpret_cast<float4 *>(base + 3 * up_a_piece() + off) =
+          make_float4(pa[0][1], pa[1][1], pa[2][1], pa[3][1]);
+    }
+  };
+  // epilogue of tile tt (TMEM buffer buf): thread = (row q*32+lane, 18 columns)
+  auto epilogue = [&](int64_t tt, int buf, int use) {
+    mbar_wait(&tm_full[buf], use & 1);
+    __syncwarp();
+    tc_fence_after();
+    const int c0 = half * 18;
+    const int64_t row = tt * kUpM + q * 32 + lane;
+    const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + buf * 256;
+    float P[18], X[18], AP[18], AX[18];
+    tmem_ld16(ta + c0, P);
+    tmem_ld2(ta + c0 + 16, P + 16);
+    tmem_ld16(ta + mp + c0, X);
+    tmem_ld2(ta + mp + c0 + 16, X + 16);
+    // A-images: leading products (+80) and cross terms (+160) accumulate in
+    // separate TMEM columns (the carried AX / AP are the drift-sensitive side)
+    {
+      float t1[18], t2[18];
+      tmem_ld16(ta + 80 + c0, t1);
+      tmem_ld2(ta + 80 + c0 + 16, t1 + 16);
+      tmem_ld16(ta + 160 + c0, t2);
+      tmem_ld2(ta + 160 + c0 + 16, t2 + 16);
+#pragma unroll
+      for (int j = 0; j < 18; ++j) AP[j] = t1[j] + t2[j];
+      tmem_ld16(ta + 80 + mp + c0, t1);
+      tmem_ld2(ta + 80 + mp + c0 + 16, t1 + 16);
+      tmem_ld16(ta + 160 + mp + c0, t2);
+      tmem_ld2(ta + 160 + mp + c0 + 16, t2 + 16);
+#pragma unroll
+      for (int j = 0; j < 18; ++j) AX[j] = t1[j] + t2[j];
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tm_empty[buf]);
+    if (row < a.n) {
+      const float br = b[row], pr = prec ? prec[row] : 1.f;
+      float W[18];
+#pragma unroll
+      for (int j = 0; j < 18; ++j) {
+        const int c = c0 + j;
+        W[j] = 0.f;
+        if (c < m) {
+          const float r = AX[j] - br * X[j] * sth[c];
+          sr[j] += r * r;
+          sx[j] += X[j] * X[j];
+          W[j] = pr * r;
+        }
+        if (c >= mp) X[j] = P[j] = W[j] = AX[j] = AP[j] = 0.f;
+      }
+      float *srow = S + row * ld, *arow = AS + row * ld, *wrow = a.wc + row * mp;
+#pragma unroll
+      for (int j = 0; j < 18; j += 2) {
+        const int c = c0 + j;
+        if (c < mp) {
+          *reinterpret_cast<float2 *>(srow + c) = make_float2(X[j], X[j + 1]);
+          *reinterpret_cast<float2 *>(srow + mp + c) = make_float2(P[j], P[j + 1]);
+          *reinterpret_cast<float2 *>(srow + 2 * mp + c) = make_float2(W[j], W[j + 1]);
+          *reinterpret_cast<float2 *>(arow + c) = make_float2(AX[j], AX[j + 1]);
+          *reinterpret_cast<float2 *>(arow + mp + c) = make_float2(AP[j], AP[j + 1]);
+          *reinterpret_cast<float2 *>(wrow + c) = make_float2(W[j], W[j + 1]);
+        }
+      }
+    }
+  };
+
+  constexpr uint32_t idesc = umma_idesc_tf32(kUpM, kUpN);
+  const uint64_t dA0 = umma_desc(0, LBO_A, SBO), dB0 = umma_desc(0, LBO_B, SBO);
+  const uint32_t zb_base = smem_u32(zb), st_base = smem_u32(st0);
+  int chunk = 0;  // global stage counter
+  if (T > 0) load_stage(t_begin * kUpM, 0);
+  for (int ti = 0; ti < T; ++ti) {
+    const int64_t tt = t_begin + ti;
+    const int buf = ti & 1;
+    for (int kc = 0; kc < nkc; ++kc, ++chunk) {
+      const int st = chunk & 1;
+      mbar_wait(&st_empty[st], ((chunk >> 1) & 1) ^ 1);  // MMAs of chunk-2 done
+      store_stage(st);
+      // prefetch the next stage (next K chunk, or chunk 0 of the next tile)
+      if (kc + 1 < nkc) load_stage(tt * kUpM, kc + 1);
+      else if (ti + 1 < T) load_stage((tt + 1) * kUpM, 0);
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        if (kc == 0) mbar_wait(&tm_empty[buf], ((ti >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const int ksteps = min(kUpKC, w - kc * kUpKC + 7) / 8;  // 8-row K steps in this stage
+        const uint32_t A = st_base + st * 4 * (uint32_t)up_a_piece();
+        const uint32_t dS = tbase + buf * 256, dA = dS + 80, dA2 = dS + 160;
+        for (int s = 0; s < ksteps; ++s) {
+          const uint32_t kb = (uint32_t)(kc * (kUpKC / 4) + 2 * s) * LBO_B;  // B: K offset
+          const uint64_t bh = dB0 | ((zb_base + kb) >> 4);
+          const uint64_t bl = dB0 | ((zb_base + (uint32_t)up_b_piece() + kb) >> 4);
+          const uint32_t ka = 2 * s * LBO_A;
+          const uint64_t sh = dA0 | ((A + ka) >> 4);
+          const uint64_t sl = dA0 | ((A + (uint32_t)up_a_piece() + ka) >> 4);
+          const uint64_t ah = dA0 | ((A + 2 * (uint32_t)up_a_piece() + ka) >> 4);
+          const uint64_t al = dA0 | ((A + 3 * (uint32_t)up_a_piece() + ka) >> 4);
+          const uint32_t acc = (kc == 0 && s == 0) ? 0u : 1u;
+          umma_tf32(dS, sl, bh, idesc, acc);  // small products first
+          umma_tf32(dS, sh, bl, idesc, 1u);
+          umma_tf32(dS, sh, bh, idesc, 1u);
+          umma_tf32(dA2, al, bh, idesc, acc);
+          umma_tf32(dA2, ah, bl, idesc, 1u);
+          umma_tf32(dA, ah, bh, idesc, acc);
+        }
+        umma_commit(&st_empty[st]);
+        if (kc == nkc - 1) umma_commit(&tm_full[buf]);
+      }
+      __syncwarp();
+      // drain the previous tile while this tile's MMAs run
+      if (kc == 0 && ti > 0) epilogue(tt - 1, buf ^ 1, (ti - 1) >> 1);
+    }
+  }
+  if (T > 0) epilogue(t_begin + T - 1, (T - 1) & 1, (T - 1) >> 1);
+  // column partials: [rn^2 (mp) | x^2 (mp)] of this CTA, reduced over its rows
+  tc_fence_before();
+  __syncthreads();
+  float *red = reinterpret_cast<float *>(st0);  // reuse the stage ring: [8 warps][2][18][32]
+  {
+#pragma unroll
+    for (int j = 0; j < 18; ++j) {
+      red[((warp * 2 + 0) * 18 + j) * 32 + lane] = sr[j];
+      red[((warp * 2 + 1) * 18 + j) * 32 + lane] = sx[j];
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < 2 * mp; c += kUpThreads) {
+    const int which = c / mp, col = c - which * mp, hf = col / 18, j = col - hf * 18;
+    double s = 0.0;
+    for (int wq = 0; wq < 4; ++wq)
+      for (int l = 0; l < 32; ++l) s += red[(((hf * 4 + wq) * 2 + which) * 18 + j) * 32 + l];
+    a.part[(size_t)blockIdx.x * 2 * mp + c] = s;
+  }
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+  }
+}
+
+// Off by default (MG_TC_UPD=1 enables it): the 2-piece split carries ~2^-22
+// relative error per product and the accumulation is not round-to-nearest,
+// so the carried X / AX drift ~1e-5 per step against the CUDA-core update's
+// ~1e-6 -- at C5 scale that costs 40-130% more LOBPCG iterations than it
+// saves per iteration (profiles/r1_tc_update.md).
+bool update_tc_supported(int w, int mp) {
+  const char *e = getenv("MG_TC_UPD");
+  if (!(e && e[0] == '1')) return false;
+  return gram_tc_supported(w) && 2 * mp <= kUpN && mp <= 40 && w <= kUpKmax;
+}
+
+int update_tc(mg_ctx *ctx, int64_t n, int ld, int w, int m, int mp, float *S, float *AS,
+              const float *b, const float *prec, const float *M, const double *theta,
+              const int *skip, double *part, float *wc) {
+  UpdTcArgs a{};
+  a.n = n;
+  a.ld = ld;
+  a.w = w;
+  a.m = m;
+  a.mp = mp;
+  a.skip = skip;
+  a.part = part;
+  a.wc = wc;
+  const int64_t ntiles = (n + kUpM - 1) / kUpM;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ctx->num_sms));
+  static thread_local bool attr = false;
+  if (!attr) {
+    MG_CUDA(cudaFuncSetAttribute(k_update_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)up_smem()));
+    attr = true;
+  }
+  k_update_tc<<<grid, kUpThreads, up_smem(), ctx->stream>>>(S, AS, b, prec, M, theta, a);
+  MG_CHECK_LAUNCH(ctx);
+  return grid;
+}
+
 template __global__ void k_gram_tc<2>(const float *, const float *, const float *, GramTcArgs);
 template __global__ void k_gram_tc<3>(const float *, const float *, const float *, GramTcArgs);
 

@@ -33,4 +33,11 @@ bool gram_tc_supported(int w);
 void gram_pair_tc(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const float *AS,
                   const float *b, double *GB, double *GA, DBuf<double> &part);
 
+// fast-path update on the tensor cores (fp32 wide blocks): P = S Zp, X = S Zx
+// (and A-images), residual W and column partials; returns the CTA count
+bool update_tc_supported(int w, int mp);
+int update_tc(mg_ctx *ctx, int64_t n, int ld, int w, int m, int mp, float *S, float *AS,
+              const float *b, const float *prec, const float *M, const double *theta,
+              const int *skip, double *part, float *wc);
+
 }  // namespace mg
