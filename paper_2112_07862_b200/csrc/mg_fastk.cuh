@@ -326,10 +326,28 @@ __global__ void __launch_bounds__(kFThreads, 1)
     for (int phase = 0; phase < 2; ++phase) {
       const int K = phase == 0 ? w : mp;
       const T *Bm = phase == 0 ? Zp : Yx;
+      // a job owns RT rows rb, rb + RS, rb + 2 RS, ... (RS = TK / RT): with
+      // the odd 16-byte row stride, 8 consecutive rb hit distinct bank groups
+      // Jobs are grouped so a warp reads at most 8 distinct 16-byte B chunks
+      // (one shared-memory wavefront): column blocks 0-7 first, then 8+.
+      const int RS = TK / RT;
+      const int nrb = TK / RT, cbA = min(cb, 8), cbB = cb - cbA;
+      const int nJA = 2 * nrb * cbA;
       for (int job = tid; job < 2 * nblk; job += kFThreads) {
-        const int mat = job / nblk, jb = job - mat * nblk;
-        const int rb = jb / cb, c0 = (jb - rb * cb) * 4;
-        const T *src = (mat ? stA(s) : stS(s)) + rb * RT * ld;
+        int mat, rb, c0;
+        if (job < nJA) {
+          mat = job / (nrb * cbA);
+          const int rem = job - mat * nrb * cbA;
+          rb = rem / cbA;
+          c0 = (rem - rb * cbA) * 4;
+        } else {
+          const int j2 = job - nJA;
+          mat = j2 / (nrb * cbB);
+          const int rem = j2 - mat * nrb * cbB;
+          rb = rem / cbB;
+          c0 = (8 + rem - rb * cbB) * 4;
+        }
+        const T *src = (mat ? stA(s) : stS(s)) + rb * ld;
         T acc[RT][4];
         if (phase == 0) {
 #pragma unroll
@@ -337,13 +355,25 @@ __global__ void __launch_bounds__(kFThreads, 1)
 #pragma unroll
             for (int y = 0; y < 4; ++y) acc[x][y] = T(0);
         } else {
-          const T *pn = (mat ? oPA : oPS) + rb * RT * mp + c0;
+          const T *pn = (mat ? oPA : oPS) + rb * mp + c0;
+          if constexpr (sizeof(T) == 4) {  // mp % 4 == 0 for fp32
 #pragma unroll
-          for (int x = 0; x < RT; ++x)
+            for (int x = 0; x < RT; ++x) {
+              const float4 v = *reinterpret_cast<const float4 *>(pn + x * RS * mp);
+              acc[x][0] = v.x;
+              acc[x][1] = v.y;
+              acc[x][2] = v.z;
+              acc[x][3] = v.w;
+            }
+          } else {
 #pragma unroll
-            for (int y = 0; y < 4; ++y) acc[x][y] = (c0 + y < mp) ? pn[x * mp + y] : T(0);
+            for (int x = 0; x < RT; ++x)
+#pragma unroll
+              for (int y = 0; y < 4; ++y) acc[x][y] = (c0 + y < mp) ? pn[x * RS * mp + y] : T(0);
+          }
         }
         if constexpr (sizeof(T) == 4) {
+#pragma unroll 3
           for (int k = 0; k < K; k += 4) {
             float4 b[4];
 #pragma unroll
@@ -351,7 +381,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
               b[kk] = *reinterpret_cast<const float4 *>(Bm + (k + kk) * mp + c0);
 #pragma unroll
             for (int x = 0; x < RT; ++x) {
-              const float4 av = *reinterpret_cast<const float4 *>(src + x * ld + k);
+              const float4 av = *reinterpret_cast<const float4 *>(src + x * RS * ld + k);
               const float aa[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
@@ -369,18 +399,25 @@ __global__ void __launch_bounds__(kFThreads, 1)
             for (int y = 0; y < 4; ++y) mz[y] = Bm[k * mp + c0 + y];
 #pragma unroll
             for (int x = 0; x < RT; ++x) {
-              const T u = src[x * ld + k];
+              const T u = src[x * RS * ld + k];
 #pragma unroll
               for (int y = 0; y < 4; ++y) acc[x][y] += u * mz[y];
             }
           }
         }
-        T *dst = (phase == 0 ? (mat ? oPA : oPS) : (mat ? oXA : oXS)) + rb * RT * mp + c0;
+        T *dst = (phase == 0 ? (mat ? oPA : oPS) : (mat ? oXA : oXS)) + rb * mp + c0;
+        if constexpr (sizeof(T) == 4) {
 #pragma unroll
-        for (int x = 0; x < RT; ++x)
+          for (int x = 0; x < RT; ++x)
+            *reinterpret_cast<float4 *>(dst + x * RS * mp) =
+                make_float4(acc[x][0], acc[x][1], acc[x][2], acc[x][3]);
+        } else {
 #pragma unroll
-          for (int y = 0; y < 4; ++y)
-            if (c0 + y < mp) dst[x * mp + y] = acc[x][y];
+          for (int x = 0; x < RT; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y)
+              if (c0 + y < mp) dst[x * RS * mp + y] = acc[x][y];
+        }
       }
       __syncthreads();
     }
