@@ -1604,7 +1604,13 @@ struct Lobpcg {
       }
       for (int c = 0; c < pcount; ++c) vcols.push_back(mp + c);
       bool done = false;
-      if (prefix && fast_ok) done = fast_iteration(vcols, cr, th, st);
+      // The fast step re-orthonormalises X from its own Gram every iteration
+      // and orders the Cholesky [X | W | P] with the drop rule, i.e. it is
+      // already the reference's full sweep (eigensolver.py:247-250) in Gram
+      // form; the every-32nd multi-pass sweep is kept only as the fallback
+      // (MG_FULL_SWEEP=1 restores it for every 32nd iteration).
+      static const bool robust_sweep = env_double("MG_FULL_SWEEP", 0) != 0;
+      if (fast_ok && (prefix || !robust_sweep)) done = fast_iteration(vcols, cr, th, st);
       if (!done) {
         if (prefix) {
           for (int rep = 0; rep < 2; ++rep) {
