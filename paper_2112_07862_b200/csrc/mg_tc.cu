@@ -806,6 +806,13 @@ void gram_pair_tc(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const f
   require(w >= 4 && w <= 112 && w % 4 == 0, MG_ERR_INTERNAL, "tc Gram: bad width");
   require(ld % 4 == 0, MG_ERR_INTERNAL, "tc Gram: row stride must be a multiple of 4");
   const int NS = tc_pieces();
+  {
+    const char *e = getenv("MG_TC_V");  // 1: the v1 converter kernel
+    if (NS == 2 && !(e && e[0] == '1') && gram_tc2_supported(w, ld)) {
+      gram_pair_tc2(ctx, n, ld, w, S, AS, b, GB, GA, part);
+      return;
+    }
+  }
   const int TK = NS == 3 ? TcCfg<3>::TK : TcCfg<2>::TK;
   const int64_t ntiles = (n + TK - 1) / TK;
   const int npairs = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ctx->num_sms / 2));

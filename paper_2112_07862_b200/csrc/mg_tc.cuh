@@ -33,6 +33,11 @@ bool gram_tc_supported(int w);
 void gram_pair_tc(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const float *AS,
                   const float *b, double *GB, double *GA, DBuf<double> &part);
 
+// v2 (mg_tc2.cu): TMA-fed, SW128 MN-major operands, one CTA per SM
+bool gram_tc2_supported(int w, int ld);
+void gram_pair_tc2(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const float *AS,
+                   const float *b, double *GB, double *GA, DBuf<double> &part);
+
 // fast-path update on the tensor cores (fp32 wide blocks): P = S Zp, X = S Zx
 // (and A-images), residual W and column partials; returns the CTA count
 bool update_tc_supported(int w, int mp);

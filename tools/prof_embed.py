@@ -1,0 +1,59 @@
+"""One device-resident embed of a config graph (for ncu launch lists / captures).
+
+    python tools/prof_embed.py [--config c5] [--n 2000000] [--reps 1]
+"""
+import argparse
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--n", type=int, default=2_000_000)
+    ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--max-iter", type=int, default=None)
+    ap.add_argument("--stats", action="store_true", help="per-class CUDA-event kernel times")
+    args = ap.parse_args()
+    import torch
+    import paper_2112_07862_b200 as mg
+    from paper_2112_07862_b200 import core, synthetic
+    cfg = synthetic.CONFIGS[args.config]
+    n, ptr, idx, w = synthetic.config_graph(cfg.name, n=args.n)
+    K = cfg.k
+    scfg = mg.SolverConfig(k=K + 1, tol=cfg.tol, max_iter=args.max_iter or cfg.max_iter, seed=42,
+                           precision=cfg.precision)
+    zh = np.random.default_rng(42).standard_normal(core._stream_size(n, max(K + 1, 8)))
+    dd = torch.device("cuda", 0)
+    dev = (torch.from_numpy(np.ascontiguousarray(ptr, np.int64)).to(dd),
+           torch.from_numpy(np.ascontiguousarray(idx, np.int64)).to(dd),
+           torch.from_numpy(np.ascontiguousarray(w, np.float64)).to(dd), torch.from_numpy(zh).to(dd))
+    from paper_2112_07862_b200 import _native as N
+    for r in range(args.reps):
+        if args.stats and r == args.reps - 1:
+            N.set_profiling(True, 0)
+            N.stats(0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res, b, dg = core.embed_arrays(n, None, None, None, K, scfg, device_inputs=dev)
+        torch.cuda.synchronize()
+        print(f"rep {r}: {time.perf_counter() - t0:.3f} s, iterations {res.iterations}, "
+              f"eps_it {dg.eps_iterations}, ev[:4] {np.asarray(res.eigenvalues)[:4]}", flush=True)
+    if args.stats:
+        st = N.stats(0)
+        N.set_profiling(False, 0)
+        for k, v in st.items():
+            if v["launches"]:
+                print(f"  {k:8s} {v['launches']:6d} launches {v['ms']:9.1f} ms "
+                      f"{1e3 * v['ms'] / v['launches']:9.1f} us/launch "
+                      f"{v['bytes'] / max(v['ms'], 1e-9) / 1e6:8.1f} GB/s", flush=True)
+
+
+if __name__ == "__main__":
+    main()
