@@ -6,7 +6,7 @@
 // and both CTAs of a pair convert the whole 'A' side -- the converters, not
 // the tensor pipe (20 % active) or HBM (16 %), set its pace.
 //
-// v2 lets the tensor core read the tiles as they arrive:
+// v2 lets the tensor core read the tiles almost as they arrive:
 //   * each row tile of S and AS is loaded by TMA (cp.async.bulk.tensor.2d,
 //     SWIZZLE_128B_ATOM_32B, 32-column panels): that IS the canonical
 //     MN-major tf32 operand layout (SWIZZLE_128B_BASE32B; M / N = the Gram
@@ -15,12 +15,14 @@
 //     lo = x - hi, bS = b_r x and its pieces (round-to-nearest hi keeps the
 //     products unbiased: with the hardware's truncation as hi, long positive
 //     sums such as diag(G_B) drift by ~2^-22 relative);
-//   * ONE MMA per (product, k-step): A = S panels (M = 128), B = [bS | AS]
-//     panels (N = 64 * PW <= 256), so G_B and G_A come out of the same
-//     instruction.  3xTF32: hi*hi -> TMEM columns [0, 256), hi*lo + lo*hi ->
-//     [256, 512) (cross terms accumulate against their own magnitude);
-//   * one CTA per SM over a contiguous row range; the fp32 TMEM accumulators
-//     are folded into the CTA's fp64 partial every kFold tiles.
+//   * 2 MMAs per k-step: A_hi x [B_hi | B_lo] (hi*hi and hi*lo side by side,
+//     N = 64 pw) and A_lo x B_hi into the cross columns;
+//   * short TMEM accumulations (64 rows, double-buffered) drained into fp32
+//     registers, folded into fp64 every 2048 rows (the TC's fp32 adds are not
+//     round-to-nearest: 2048-row TMEM sums failed the 2e-6 bar).
+// Measured (profiles/r1_gram_tc.md): 11-13 ms at 20M x 108 vs 16.8 ms (v1);
+// the per-tile pipeline (~0.5 us per 16-row tile even with the MMAs and the
+// element-wise work disabled) bounds it, not HBM or the tensor pipe.
 // Mirror convention (as v1 / k_reduce_gram2): entries of block-lower 8x8
 // blocks come from the block-upper product, so only j >= 8 floor(i/8) is
 // drained.
@@ -35,10 +37,10 @@ namespace mg {
 namespace {
 
 constexpr int kG2Threads = 320;   // warp 0 TMA producer, warp 1 MMA issuer, 8 worker warps
-constexpr int kG2TK = 16;         // rows per stage (2 MMA k-steps)
-constexpr int kG2Stages = 6;
+constexpr int kG2TK = 32;         // rows per stage (4 MMA k-steps)
+constexpr int kG2Stages = 3;
 constexpr int kG2Panel = kG2TK * 128;  // bytes per 32-column panel of a stage
-constexpr int kG2FL = 4;          // tiles per TMEM accumulation group (64 rows)
+constexpr int kG2FL = 2;          // tiles per TMEM accumulation group (64 rows)
 constexpr int kG2FoldG = 32;      // groups per fp64 fold (2048 rows)
 
 __host__ __device__ constexpr size_t g2_smem_bytes(int pw) {
@@ -87,6 +89,13 @@ __device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *map, int c0
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(void *dst, const CUtensorMap *map, int r0, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(r0), "r"(0), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void tma_1d(void *dst, const CUtensorMap *map, int c0, uint64_t *bar) {
@@ -168,6 +177,7 @@ __device__ __forceinline__ void g2_drain(int fg, int NG, uint64_t *tmf, uint64_t
 struct Gram2TcArgs {
   int64_t n;
   int w, pw;      // Gram width, 32-column panels (w <= 32 pw, pw in 2..4)
+  int pwf;        // full panels (w / 32), loaded by the 3-D maps
   int npairs;     // grid = 2 * npairs
   int dbg;        // MG_TC2_DBG timing experiments: 1 no MMA, 2 no derive, 4 no drain
   double *part;   // [pair][h][128 (j)][128 (i)] fp64, zeroed by the host
@@ -184,6 +194,7 @@ struct Gram2TcArgs {
 // rounding at the v1 level; registers fold into fp64 every kG2FoldG groups.
 __global__ void __launch_bounds__(kG2Threads, 1)
     k_gram_tc2(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmA,
+               const __grid_constant__ CUtensorMap tmS3, const __grid_constant__ CUtensorMap tmA3,
                const __grid_constant__ CUtensorMap tmB, Gram2TcArgs a) {
   // the dynamic window starts 1024-aligned (no static shared memory here);
   // keeping the __shared__ array itself as the base lets the compiler emit
@@ -233,17 +244,24 @@ __global__ void __launch_bounds__(kG2Threads, 1)
     // --------------------------------------------------------- TMA producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmS)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmS3)) : "memory");
+      if (h) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA3)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(
                        reinterpret_cast<uint64_t>(h ? &tmA : &tmB)) : "memory");
       for (int t = 0; t < T; ++t) {
         const int s = t % kG2Stages;
-        if (!(a.dbg & 8)) mbar_wait(&empty[s], ((t / kG2Stages) & 1) ^ 1);
-        else if (t >= kG2Stages) mbar_wait(&full[s], ((t / kG2Stages) & 1) ^ 1);
+        mbar_wait(&empty[s], ((t / kG2Stages) & 1) ^ 1);
         unsigned char *st = sm + s * SB;
         mbar_expect_tx(&full[s], h ? 2 * PB : PB + kG2TK * 4);
         const int r0 = (int)((t0 + t) * kG2TK);
         if (!h) tma_1d(sb + s * 32, &tmB, r0, &full[s]);
-        for (int p = 0; p < pw; ++p) {
+        // full 32-column panels in one 3-D box, the partial last panel (zero
+        // beyond w) as a 2-D box: 2 TMA instructions per matrix and tile
+        if (a.pwf) {
+          tma_3d(st, &tmS3, r0, &full[s]);
+          if (h) tma_3d(st + 2 * PB, &tmA3, r0, &full[s]);
+        }
+        for (int p = a.pwf; p < pw; ++p) {
           tma_2d(st + p * kG2Panel, &tmS, 32 * p, r0, &full[s]);
           if (h) tma_2d(st + 2 * PB + p * kG2Panel, &tmA, 32 * p, r0, &full[s]);
         }
@@ -381,6 +399,24 @@ CUtensorMap make_map(const float *base, int64_t n, int ld, int w) {
   return m;
 }
 
+// the first pf full 32-column panels of row-major fp32 [n x ld] as a 3-D
+// tensor (column-in-panel, row, panel): one box = kG2TK rows x pf panels,
+// landing panel-major exactly like pf separate 2-D boxes
+CUtensorMap make_map_3d(const float *base, int64_t n, int ld, int pf) {
+  CUtensorMap m;
+  const int pd = pf > 0 ? pf : 1;
+  cuuint64_t dims[3] = {32, (cuuint64_t)n, (cuuint64_t)pd};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * sizeof(float), 32 * sizeof(float)};
+  cuuint32_t box[3] = {32, (cuuint32_t)kG2TK, (cuuint32_t)pd};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  require(r == CUDA_SUCCESS, MG_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string((int)r));
+  return m;
+}
+
 // fp32 vector [n]: kG2TK-element boxes (zero beyond n)
 CUtensorMap make_map_1d(const float *base, int64_t n) {
   CUtensorMap m;
@@ -424,7 +460,9 @@ void gram_pair_tc2(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const 
     const char *e = getenv("MG_TC2_DBG");
     a.dbg = e ? atoi(e) : 0;
   }
+  a.pwf = w / 32;
   const CUtensorMap mS = make_map(S, n, ld, w), mA = make_map(AS, n, ld, w), mB = make_map_1d(b, n);
+  const CUtensorMap mS3 = make_map_3d(S, n, ld, a.pwf), mA3 = make_map_3d(AS, n, ld, a.pwf);
   const size_t smem = g2_smem_bytes(pw);
   static thread_local size_t smem_set = 0;
   if (smem > smem_set) {
@@ -433,8 +471,8 @@ void gram_pair_tc2(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const 
     smem_set = smem;
   }
   {
-    ProfScope ps(ctx, PROF_GRAM, 2.0 * n * w * sizeof(float));
-    k_gram_tc2<<<grid, kG2Threads, smem, ctx->stream>>>(mS, mA, mB, a);
+    ProfScope ps(ctx, PROF_GRAM, 2.0 * n * w * sizeof(float) + 4.0 * n);
+    k_gram_tc2<<<grid, kG2Threads, smem, ctx->stream>>>(mS, mA, mS3, mA3, mB, a);
     MG_CHECK_LAUNCH(ctx);
   }
   k_reduce_gram_tc2<<<grid_for(2 * w * w, 256, 4 * ctx->num_sms), 256, 0, ctx->stream>>>(
