@@ -1255,6 +1255,7 @@ struct Lobpcg {
         break;
       }
     if (!tk_upd) return;
+    if (const char *e = getenv("MG_UPD_TK")) tk_upd = std::min(tk_upd, atoi(e));
     const int cb = (mp + 3) / 4;
     // tallest register block that still keeps >= 3/4 of the threads busy
     rt_upd = 2;
@@ -1263,6 +1264,7 @@ struct Lobpcg {
         rt_upd = rt;
         break;
       }
+    if (const char *e = getenv("MG_UPD_RT")) rt_upd = atoi(e);
     gram2_smem = gram2_bytes(tk_gram, ns_gram);
     upd_smem = upd_bytes(tk_upd, 3);
     int smax = m + 2 * m;
@@ -1599,7 +1601,18 @@ struct Lobpcg {
         spmm_cols(0, 3 * mp);
       } else {
         halo(Wc.p, mp);
-        spmm<T>(ctx, A, Wc.p, mp, AS.p + 2 * mp, ld, mp);  // compact W: L2-resident gathers
+        // soft locking (eigensolver.py:235-238): only active columns of W enter
+        // the basis; they usually form a suffix (the smallest pairs converge
+        // first), so A W is formed for the 16-byte-aligned column range that
+        // covers them -- the images of locked columns are never read
+        int c0 = m;
+        for (int c = 0; c < m; ++c)
+          if (!cv[c]) {
+            c0 = c;
+            break;
+          }
+        c0 = c0 / VN * VN;
+        spmm<T>(ctx, A, Wc.p + c0, mp, AS.p + 2 * mp + c0, ld, mp - c0);
         debug_check("spmm");
       }
       for (int c = 0; c < pcount; ++c) vcols.push_back(mp + c);
