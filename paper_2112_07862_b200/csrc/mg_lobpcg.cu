@@ -91,6 +91,7 @@ void make_solver_csr(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *
     MG_CHECK_LAUNCH(ctx);
     out.view.rowsum = out.rowsum.p;
   }
+  build_blocked<T>(ctx, out);
 }
 
 // ------------------------------------------------------------------ SpMM ---
@@ -233,6 +234,7 @@ void spmm(mg_ctx *ctx, const DevCSR<T> &A, const T *X, int ldx, T *Y, int ldy, i
   double bytes = (double)A.nnz * (sizeof(T) + sizeof(int)) + 8.0 * (A.n + 1) +
                  2.0 * sizeof(T) * (double)A.n * w;
   ProfScope ps(ctx, PROF_SPMM, bytes);
+  if (spmm_staged<T>(ctx, A, X, ldx, Y, ldy, w)) return;
   if (A.rowsum)
     k_spmm<T, true><<<grid, 256, 0, ctx->stream>>>(A.n, A.ptr, A.idx, A.val, X, ldx, Y, ldy, L,
                                                    A.rowsum);
