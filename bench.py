@@ -95,6 +95,19 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def ncu_traffic(cfgname, n, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of ``kernel`` from the
+    committed ncu --set full summary (profiles/ncu_traffic.json), when it was
+    captured on this config; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh)
+        e = d[f"{cfgname}_{n}"][kernel]
+        return float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -344,7 +357,8 @@ def main():
                    "seconds_solve": dg.seconds_solve, "graph_build_s": t_graph},
         "roofline": {"kernel": "k_spmm (CSR x row-major block, A*W)", "bound": "hbm",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm if hbm else None, "traffic": None,
+                     "frac": achieved / hbm if hbm else None,
+                     "traffic": ncu_traffic(cfg.name, n, "k_spmm"),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": spmm_bytes, "avg_launch_ms": spmm_ms},
         "kernels": kern,

@@ -220,6 +220,32 @@ int mg_embed_host(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *
 int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float *S,
                      const float *AS, const float *b, double *GB, double *GA);
 
+/* --------------------------------------- kNN graph -------
+ * knn_graph (graph.py:281-315): symmetrized k-nearest-neighbour graph of the
+ * rows of X (device n x d row-major fp64), ties at the k-th distance to the
+ * lower index, Gaussian weights exp(-d^2 / sigma^2) with sigma^2 the mean
+ * squared distance over the retained edges (weighted != 0), else 1; output
+ * in the canonical CSR of Graph.from_edges (graph.py:31-79).  Two-phase:
+ * _count fills indptr (device int64[n+1]) and *nnz (host); _fill writes
+ * indices (device int64[nnz]) and weights (device double[nnz]).
+ * k <= 64, d <= 5120; O(n^2 d) like the reference. */
+int mg_knn_graph_count(mg_ctx *ctx, int64_t n, int32_t d, const double *X, int32_t k,
+                       int32_t weighted, int64_t *indptr, int64_t *nnz);
+int mg_knn_graph_fill(mg_ctx *ctx, int64_t n, int32_t d, const double *X, int32_t k,
+                      int32_t weighted, int64_t *indices, double *weights);
+
+/* ------------------------------------------ clustering ---
+ * The C4 readout after the embedding: device k-means with the reference's
+ * portable seeding streams.  points: device n x d row-major fp64. */
+/* kmeans (clustering.py:99-134; k-means++ :57-67, Lloyd :70-96, streams
+ * rng.py:9-127): best of `restarts` restarts from xoshiro256** streams
+ * stream_seed(seed, r); labels: device int64[n]; wcss: host, may be NULL.
+ * d <= 32, c <= 64, c * d <= 512. */
+int mg_kmeans(mg_ctx *ctx, int64_t n, int32_t d, const double *points, int32_t c,
+              int32_t restarts, uint64_t seed, int64_t *labels, double *wcss);
+/* normalize_rows (clustering.py:50-56): unit Euclidean rows, zero rows kept */
+int mg_normalize_rows(mg_ctx *ctx, int64_t n, int32_t d, const double *points, double *out);
+
 /* ---------------------------------------------------- multi-GPU (8(e)) ---
  * 1-D row partition of the solve over ranks (one process per GPU).  The
  * setup (Q, eps, mu, A, b) is replicated; each LOBPCG SpMM exchanges halo

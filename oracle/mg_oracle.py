@@ -28,6 +28,7 @@ __all__ = [
     "gershgorin_radii", "balance_radii", "degree_balancing", "operator_pair",
     "pair_diagnostics", "lobpcg", "smallest_above_null", "embed",
     "laplacian_eigenmaps", "dense_generalized_eigh", "initial_block",
+    "Xoshiro256", "stream_seed", "normalize_rows", "kmeans", "knn_graph",
 ]
 
 DROP_REL = 1e-12          # eigensolver.py:29
@@ -562,3 +563,149 @@ def dense_generalized_eigh(a: CSR, b, k):
     c = a.dense() * s[:, None] * s[None, :]
     w, v = np.linalg.eigh(0.5 * (c + c.T))
     return w[:k], _signs(s[:, None] * v[:, :k])
+
+
+# ------------------------------------------------------------ clustering ---
+# C4 readout: rng.py:9-127 and clustering.py:50-134.
+_M64 = (1 << 64) - 1
+
+
+def _mix64(x):
+    """rng.py:49-54 (splitmix64 finalizer)."""
+    x &= _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return (x ^ (x >> 31)) & _M64
+
+
+def stream_seed(seed, index):
+    """rng.py:65-67."""
+    return _mix64((_mix64(seed) + ((index + 1) * 0xD2B74407B1CE6E93 & _M64)) & _M64)
+
+
+class Xoshiro256:
+    """rng.py:74-127 (xoshiro256** seeded by four splitmix64 outputs)."""
+
+    def __init__(self, seed):
+        z, s = seed & _M64, []
+        for _ in range(4):
+            z = (z + 0x9E3779B97F4A7C15) & _M64
+            s.append(_mix64(z))
+        if not any(s):
+            s[0] = 1
+        self.s = s
+
+    def next_u64(self):
+        s0, s1, s2, s3 = self.s
+        rot = lambda x, r: ((x << r) | (x >> (64 - r))) & _M64  # noqa: E731
+        out = (rot((s1 * 5) & _M64, 7) * 9) & _M64
+        t = (s1 << 17) & _M64
+        s2 ^= s0
+        s3 ^= s1
+        s1 ^= s2
+        s0 ^= s3
+        s2 ^= t
+        self.s = [s0, s1, s2, rot(s3, 45)]
+        return out
+
+    def uniform(self):
+        return (self.next_u64() >> 11) * (2.0 ** -53)
+
+    def index(self, n):
+        i = int(self.uniform() * n)
+        return n - 1 if i >= n else i
+
+    def weighted_index(self, cum):
+        total = float(cum[-1])
+        if total <= 0.0:
+            return self.index(len(cum))
+        return int(np.searchsorted(cum, self.uniform() * total, side="right"))
+
+
+def normalize_rows(pts):
+    """clustering.py:50-56."""
+    pts = np.asarray(pts, np.float64)
+    nr = np.linalg.norm(pts, axis=1, keepdims=True)
+    return np.where(nr > 0.0, pts / np.where(nr > 0.0, nr, 1.0), pts)
+
+
+def kmeans(pts, c, restarts=20, seed=42):
+    """clustering.py:99-134 (k-means++ :57-67, Lloyd :70-96); returns (labels, wcss)."""
+    pts = np.asarray(pts, np.float64)
+    if pts.ndim == 1:
+        pts = pts[:, None]
+    n = pts.shape[0]
+    if not 1 <= c <= n or restarts < 1:
+        raise OracleInputError("bad cluster count / restarts")
+    if c == 1:
+        return np.zeros(n, np.int64), 0.0
+    if c == n:
+        return np.arange(n, dtype=np.int64), 0.0
+    best = None
+    for r in range(restarts):
+        rng = Xoshiro256(stream_seed(seed, r))
+        centers = np.empty((c, pts.shape[1]))
+        centers[0] = pts[rng.index(n)]
+        d2 = np.sum((pts - centers[0]) ** 2, axis=1)
+        for j in range(1, c):
+            centers[j] = pts[rng.weighted_index(np.cumsum(d2))]
+            d2 = np.minimum(d2, np.sum((pts - centers[j]) ** 2, axis=1))
+        labels = np.full(n, -1, dtype=np.int64)
+        for _ in range(300):
+            dd = (np.sum(pts * pts, axis=1)[:, None] - 2.0 * (pts @ centers.T)
+                  + np.sum(centers * centers, axis=1)[None, :])
+            new = np.argmin(dd, axis=1)
+            for j in range(c):
+                if not np.any(new == j):
+                    fit = dd[np.arange(n), new]
+                    fit = np.where(np.bincount(new, minlength=c)[new] > 1, fit, -np.inf)
+                    new[int(np.argmax(fit))] = j
+            if np.array_equal(new, labels):
+                break
+            labels = new
+            for j in range(c):
+                mem = pts[labels == j]
+                if mem.size:
+                    centers[j] = mem.mean(axis=0)
+        wcss = float(np.sum((pts - centers[labels]) ** 2))
+        if best is None or wcss < best[1]:
+            best = (labels, wcss)
+    return best
+
+
+def knn_graph(X, k, weighted=True):
+    """graph.py:281-315 (dense distances, stable argsort, union, mean-d2 bandwidth)
+    -> canonical CSR (graph.py:31-79); returns (n, indptr, indices, weights)."""
+    X = np.asarray(X, dtype=np.float64)
+    if X.ndim != 2:
+        raise OracleInputError("feature matrix must be 2-D")
+    n = X.shape[0]
+    if not 1 <= k < n:
+        raise OracleInputError(f"k must satisfy 1 <= k < n, got k={k}, n={n}")
+    sq = np.sum(X * X, axis=1)
+    d2 = sq[:, None] + sq[None, :] - 2.0 * (X @ X.T)
+    np.maximum(d2, 0.0, out=d2)
+    np.fill_diagonal(d2, np.inf)
+    nearest = np.argsort(d2, axis=1, kind="stable")[:, :k]
+    i = np.repeat(np.arange(n), k)
+    j = nearest.ravel()
+    key = np.unique(np.minimum(i, j) * n + np.maximum(i, j))
+    ii, jj = key // n, key % n
+    if weighted:
+        dist2 = d2[ii, jj]
+        sigma2 = float(dist2.mean())
+        w = np.exp(-dist2 / sigma2) if sigma2 > 0.0 else np.ones_like(dist2)
+    else:
+        w = np.ones(key.size)
+    bad = ~((w > 0.0) & np.isfinite(w))
+    if np.any(bad):
+        e = int(np.argmax(bad))
+        raise OracleInputError(f"edge ({ii[e]}, {jj[e]}) has non-positive weight {w[e]}")
+    src = np.concatenate([ii, jj])
+    dst = np.concatenate([jj, ii])
+    wts = np.concatenate([w, w])
+    order = np.lexsort((dst, src))
+    indptr = np.zeros(n + 1, np.int64)
+    np.add.at(indptr, src[order] + 1, 1)
+    np.cumsum(indptr, out=indptr)
+    return n, indptr, dst[order], wts[order]

@@ -34,6 +34,8 @@ from .core import (  # noqa: F401
     two_hop_laplacian,
     two_hop_sets,
 )
+from .clustering import kmeans, normalize_rows  # noqa: F401
+from .knn import knn_graph  # noqa: F401
 from .errors import (  # noqa: F401
     ConvergenceError,
     DisconnectedGraphError,

@@ -9,6 +9,8 @@
 #include "mg_comm.cuh"
 #include "mg_dist.cuh"
 #include "mg_tc.cuh"
+#include "mg_kmeans.cuh"
+#include "mg_knn.cuh"
 #include "mg_graph.cuh"
 #include "mg_small.cuh"
 
@@ -710,6 +712,49 @@ int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float 
           "tensor-core Gram pair needs 64 < w <= 128 (set MG_TC=1)");
   DBuf<double> part;
   gram_pair_tc(ctx, n, ld, w, S, AS, b, GB, GA, part);
+  sync(ctx);
+  MG_API_END
+}
+
+int mg_knn_graph_count(mg_ctx *ctx, int64_t n, int32_t d, const double *X, int32_t k,
+                       int32_t weighted, int64_t *indptr, int64_t *nnz) {
+  MG_API_BEGIN(ctx)
+  require(X != nullptr && indptr != nullptr && nnz != nullptr, MG_ERR_INPUT, "NULL argument");
+  KnnResult r = knn_graph(ctx, n, d, X, k, weighted != 0);
+  MG_CUDA(cudaMemcpyAsync(indptr, r.indptr.p, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  *nnz = r.nnz;
+  sync(ctx);
+  MG_API_END
+}
+
+int mg_knn_graph_fill(mg_ctx *ctx, int64_t n, int32_t d, const double *X, int32_t k,
+                      int32_t weighted, int64_t *indices, double *weights) {
+  MG_API_BEGIN(ctx)
+  require(X != nullptr && indices != nullptr && weights != nullptr, MG_ERR_INPUT, "NULL argument");
+  KnnResult r = knn_graph(ctx, n, d, X, k, weighted != 0);
+  if (r.nnz) {
+    MG_CUDA(cudaMemcpyAsync(indices, r.indices.p, r.nnz * sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    MG_CUDA(cudaMemcpyAsync(weights, r.weights.p, r.nnz * sizeof(double), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+  }
+  sync(ctx);
+  MG_API_END
+}
+
+int mg_kmeans(mg_ctx *ctx, int64_t n, int32_t d, const double *points, int32_t c,
+              int32_t restarts, uint64_t seed, int64_t *labels, double *wcss) {
+  MG_API_BEGIN(ctx)
+  require(points != nullptr && labels != nullptr, MG_ERR_INPUT, "points / labels is NULL");
+  const double v = kmeans(ctx, n, d, points, c, restarts, seed, labels);
+  if (wcss) *wcss = v;
+  MG_API_END
+}
+
+int mg_normalize_rows(mg_ctx *ctx, int64_t n, int32_t d, const double *points, double *out) {
+  MG_API_BEGIN(ctx)
+  normalize_rows(ctx, n, d, points, out);
   sync(ctx);
   MG_API_END
 }

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
   unsigned char *after = reinterpret_cast<unsigned char *>(sprec + TK + 4);
   after = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(after) + 15) & ~uintptr_t(15));
   uint64_t *bars = reinterpret_cast<uint64_t *>(after);
-  double *red = reinterpret_cast<double *>(after + 64);     // [kFThreads][2]
+  double *red = reinterpret_cast<double *>(after + 64);     // [kFThreads][8]
 
   const int tid = threadIdx.x;
   for (int e = tid; e < mlen; e += kFThreads) sM[e] = Mg[e];
@@ -312,6 +312,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
   const int R = kFThreads / mp;
   const int rc = tid % mp, rrow = tid / mp;
   double sr = 0.0, sx = 0.0;
+  // fp32 residual pass: 16-byte chunks (mp % 4 == 0)
+  const int C4 = mp / 4, R4 = kFThreads / (C4 > 0 ? C4 : 1);
+  const int rc4 = tid % (C4 > 0 ? C4 : 1), rrow4 = tid / (C4 > 0 ? C4 : 1);
+  double sr4[4] = {0.0, 0.0, 0.0, 0.0}, sx4[4] = {0.0, 0.0, 0.0, 0.0};
   const T *Zp = sM, *Yx = sM + w * mp;
   const int cb = (mp + 3) / 4, nblk = (TK / RT) * cb;  // per matrix
   for (int64_t t = t_begin; t < t_end; ++t) {
@@ -422,25 +426,57 @@ __global__ void __launch_bounds__(kFThreads, 1)
       __syncthreads();
     }
     // residual + W, and write back [X P W] / [AX AP] rows
-    for (int rr = rrow; rr < nr && rrow < R; rr += R) {
-      const T x = oXS[rr * mp + rc];
-      const T ax = oXA[rr * mp + rc];
-      T wv = T(0);
-      if (rc < a.m) {
-        const T bx = stB(s)[rr] * x;
-        const T r = ax - bx * sth[rc];
-        sr += (double)r * (double)r;
-        sx += (double)x * (double)x;
-        wv = sprec[rr] * r;
+    if constexpr (sizeof(T) == 4) {
+      // one 16-byte column chunk per thread (fixed chunk: rows rr4, rr4 + R4, ...)
+      for (int rr = rrow4; rr < nr && rrow4 < R4; rr += R4) {
+        const float4 x = *reinterpret_cast<const float4 *>(oXS + rr * mp + 4 * rc4);
+        const float4 ax = *reinterpret_cast<const float4 *>(oXA + rr * mp + 4 * rc4);
+        const float xs[4] = {x.x, x.y, x.z, x.w}, axs[4] = {ax.x, ax.y, ax.z, ax.w};
+        const float br = stB(s)[rr], pr = sprec[rr];
+        float wv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          wv[q] = 0.f;
+          if (4 * rc4 + q < a.m) {
+            const float r = axs[q] - br * xs[q] * sth[4 * rc4 + q];
+            sr4[q] += (double)r * (double)r;
+            sx4[q] += (double)xs[q] * (double)xs[q];
+            wv[q] = pr * r;
+          }
+        }
+        const float4 w4 = make_float4(wv[0], wv[1], wv[2], wv[3]);
+        float *srow = S + (r0 + rr) * ld + 4 * rc4;
+        float *arow = AS + (r0 + rr) * ld + 4 * rc4;
+        *reinterpret_cast<float4 *>(srow) = x;
+        *reinterpret_cast<float4 *>(srow + mp) =
+            *reinterpret_cast<const float4 *>(oPS + rr * mp + 4 * rc4);
+        *reinterpret_cast<float4 *>(srow + 2 * mp) = w4;
+        reinterpret_cast<float4 *>(reinterpret_cast<float *>(a.wc) + (r0 + rr) * mp)[rc4] = w4;
+        *reinterpret_cast<float4 *>(arow) = ax;
+        *reinterpret_cast<float4 *>(arow + mp) =
+            *reinterpret_cast<const float4 *>(oPA + rr * mp + 4 * rc4);
       }
-      T *srow = S + (r0 + rr) * ld;
-      T *arow = AS + (r0 + rr) * ld;
-      srow[rc] = x;
-      srow[mp + rc] = oPS[rr * mp + rc];
-      srow[2 * mp + rc] = wv;
-      reinterpret_cast<T *>(a.wc)[(r0 + rr) * mp + rc] = wv;
-      arow[rc] = ax;
-      arow[mp + rc] = oPA[rr * mp + rc];
+    } else {
+      for (int rr = rrow; rr < nr && rrow < R; rr += R) {
+        const T x = oXS[rr * mp + rc];
+        const T ax = oXA[rr * mp + rc];
+        T wv = T(0);
+        if (rc < a.m) {
+          const T bx = stB(s)[rr] * x;
+          const T r = ax - bx * sth[rc];
+          sr += (double)r * (double)r;
+          sx += (double)x * (double)x;
+          wv = sprec[rr] * r;
+        }
+        T *srow = S + (r0 + rr) * ld;
+        T *arow = AS + (r0 + rr) * ld;
+        srow[rc] = x;
+        srow[mp + rc] = oPS[rr * mp + rc];
+        srow[2 * mp + rc] = wv;
+        reinterpret_cast<T *>(a.wc)[(r0 + rr) * mp + rc] = wv;
+        arow[rc] = ax;
+        arow[mp + rc] = oPA[rr * mp + rc];
+      }
     }
     __syncthreads();  // stage s and the output tiles are free
     if (tid == 0 && t + NS < t_end) {
@@ -448,14 +484,29 @@ __global__ void __launch_bounds__(kFThreads, 1)
       issue_tile<T>(S, AS, b, a.n, ld, TK, t + NS, stS(s), stA(s), stB(s), &bars[s]);
     }
   }
-  red[tid * 2] = (rrow < R) ? sr : 0.0;
-  red[tid * 2 + 1] = (rrow < R) ? sx : 0.0;
-  __syncthreads();
-  for (int c = tid; c < 2 * mp; c += kFThreads) {
-    const int col = c % mp, which = c / mp;
-    double s2 = 0.0;
-    for (int q = 0; q < R; ++q) s2 += red[(q * mp + col) * 2 + which];
-    a.part[(size_t)blockIdx.x * 2 * mp + c] = s2;
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      red[tid * 8 + q] = (rrow4 < R4) ? sr4[q] : 0.0;
+      red[tid * 8 + 4 + q] = (rrow4 < R4) ? sx4[q] : 0.0;
+    }
+    __syncthreads();
+    for (int c = tid; c < 2 * mp; c += kFThreads) {
+      const int col = c % mp, which = c / mp;
+      double s2 = 0.0;
+      for (int q = 0; q < R4; ++q) s2 += red[(q * C4 + col / 4) * 8 + 4 * which + (col & 3)];
+      a.part[(size_t)blockIdx.x * 2 * mp + c] = s2;
+    }
+  } else {
+    red[tid * 2] = (rrow < R) ? sr : 0.0;
+    red[tid * 2 + 1] = (rrow < R) ? sx : 0.0;
+    __syncthreads();
+    for (int c = tid; c < 2 * mp; c += kFThreads) {
+      const int col = c % mp, which = c / mp;
+      double s2 = 0.0;
+      for (int q = 0; q < R; ++q) s2 += red[(q * mp + col) * 2 + which];
+      a.part[(size_t)blockIdx.x * 2 * mp + c] = s2;
+    }
   }
 }
 

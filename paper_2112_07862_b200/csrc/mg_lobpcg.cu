@@ -1105,7 +1105,7 @@ struct Lobpcg {
     ca.use_global = ug;
     ca.rel_tol = rel_tol();
     ca.abs_tol = sizeof(T) == 8 ? 1e-12 : 1e-7;
-    if (sm > 48 * 1024)
+    if (sm > 0)  // static + dynamic may exceed 48 KB even when the dynamic part does not
       MG_CUDA(cudaFuncSetAttribute(k_ctrl_chol<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)sm));
     k_ctrl_chol<T><<<1, kCtrlThreads, sm, ctx->stream>>>(ca, Gr0.p, M.p, status.p, scratch.p);
@@ -1126,7 +1126,7 @@ struct Lobpcg {
     ra.use_global = need > 200 * 1024;
     ra.rel_tol = rel_tol();
     size_t sm = ra.use_global ? 0 : need;
-    if (sm > 48 * 1024)
+    if (sm > 0)  // static + dynamic may exceed 48 KB even when the dynamic part does not
       MG_CUDA(cudaFuncSetAttribute(k_ctrl_rr<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)sm));
     k_ctrl_rr<T><<<1, kCtrlThreads, sm, ctx->stream>>>(ra, Gr0.p, Gr1.p, M.p, theta.p, status.p,
@@ -1230,7 +1230,7 @@ struct Lobpcg {
     const size_t mlen = (size_t)w * mp + (size_t)mp * mp;
     return (size_t)ns * (2 * ((size_t)tk * ld + 16) + tk + 16) * sizeof(T) +
            (mlen + 16 + 4 * (size_t)tk * mp + mp + 4 + tk + 4) * sizeof(T) + 16 + 64 +
-           (size_t)kFThreads * 2 * sizeof(double) + 64;
+           (size_t)kFThreads * 8 * sizeof(double) + 64;
   }
 
   void fast_setup() {
@@ -1283,7 +1283,7 @@ struct Lobpcg {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget));
     MG_CUDA(cudaFuncSetAttribute(k_update_resid<T, 3, 2>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget));
-    if (fast_smem > 48 * 1024)
+    if (fast_smem > 0)  // k_ctrl_fast has ~28 KB of static shared memory too
       MG_CUDA(cudaFuncSetAttribute(k_ctrl_fast<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)fast_smem));
     int64_t ntile = (n + tk_gram - 1) / tk_gram;
