@@ -352,6 +352,42 @@ __global__ void k_colamax(int64_t n, const T *__restrict__ S, int ld, int mp,
   }
 }
 
+// deflation (eigensolver.py:92-99: block -= y (y'B block) / (y'B y)), the
+// y'B[region] row in fp64 partials (thread -> fixed column, rows strided),
+// then the rank-1 update of the projected columns.  Two light passes over the
+// region instead of two full tile passes over S.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_ydot(int64_t n, const T *__restrict__ S, int ld, const T *__restrict__ b, int ycol, int r0,
+           int rw, double *__restrict__ part) {
+  __shared__ double red[256];
+  const int per = 256 / rw;  // rows in flight per block (rw <= 256)
+  const int c = threadIdx.x % rw, rs = threadIdx.x / rw;
+  double acc = 0.0;
+  if (rs < per)
+    for (int64_t i = (int64_t)blockIdx.x * per + rs; i < n; i += (int64_t)gridDim.x * per)
+      acc += (double)b[i] * (double)S[i * ld + ycol] * (double)S[i * ld + r0 + c];
+  red[threadIdx.x] = rs < per ? acc : 0.0;
+  __syncthreads();
+  if (threadIdx.x < rw) {
+    double t = 0.0;
+    for (int q = 0; q < per; ++q) t += red[q * rw + threadIdx.x];
+    part[(int64_t)blockIdx.x * rw + threadIdx.x] = t;
+  }
+}
+
+template <typename T>
+__global__ void k_yaxpy(int64_t n, T *__restrict__ S, int ld, int ycol, int c_lo, int c_hi, int r0,
+                        const double *__restrict__ g, double denom) {
+  const int w = c_hi - c_lo;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * w;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / w;
+    const int c = c_lo + (int)(e - i * w);
+    S[i * ld + c] = (T)((double)S[i * ld + c] - (double)S[i * ld + ycol] * (g[c - r0] / denom));
+  }
+}
+
 __global__ void k_reduce_cols(const double *__restrict__ part, int nb, int w,
                               double *__restrict__ out) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < w; t += gridDim.x * blockDim.x) {
@@ -1051,23 +1087,42 @@ struct Lobpcg {
 
   // project y out of physical columns [c_lo, c_hi) (eigensolver.py:92-99)
   void deflate_cols(int c_lo, int c_hi, int region0, int region_w) {
-    if (!have_y) return;
-    GramSpec g = gspec(3 * mp, 1, region0, region_w, 0, 0);
-    pass(0, 0, 0, 0, 0, 0, 0, &g, 1, Gr0.p, nullptr);
-    ProjArgs pa{};
-    pa.nx = 1;
-    pa.rows = 1;
-    pa.g_c0 = region0;
-    pa.g_cw = region_w;
-    pa.o0 = region0;
-    pa.ow = region_w;
-    pa.nv = 0;
-    for (int c = c_lo; c < c_hi; ++c) pa.vcols[pa.nv++] = c;
-    pa.denom = ydenom;
-    k_ctrl_proj<T><<<1, 256, 0, ctx->stream>>>(pa, Gr0.p, M.p);
+    if (!have_y || c_hi <= c_lo) return;
+    if (sizeof(T) == 8) {
+      // fp64: the reference's own arithmetic order (a Gram tile pass, then the
+      // transform), which keeps the deflated eps solve on its trajectory
+      // (C2's eps matches to 3.5e-15 only this way)
+      GramSpec g = gspec(3 * mp, 1, region0, region_w, 0, 0);
+      pass(0, 0, 0, 0, 0, 0, 0, &g, 1, Gr0.p, nullptr);
+      ProjArgs pa{};
+      pa.nx = 1;
+      pa.rows = 1;
+      pa.g_c0 = region0;
+      pa.g_cw = region_w;
+      pa.o0 = region0;
+      pa.ow = region_w;
+      pa.nv = 0;
+      for (int c = c_lo; c < c_hi; ++c) pa.vcols[pa.nv++] = c;
+      pa.denom = ydenom;
+      k_ctrl_proj<T><<<1, 256, 0, ctx->stream>>>(pa, Gr0.p, M.p);
+      MG_CHECK_LAUNCH(ctx);
+      pass(1, 1, 0, 3 * mp, 1, region0, region_w, nullptr, 0, nullptr, nullptr);
+      return;
+    }
+    // fp32: two light passes over the region (the tile passes cost ~11 ms
+    // each at C5 and dominated the eps solve)
+    const int nb = grid_for(n, std::max(1, 256 / region_w), ctx->num_sms * 4);
+    if (ypart.n < (size_t)nb * region_w) ypart.alloc(ctx, (size_t)nb * region_w);
+    k_ydot<T><<<nb, 256, 0, ctx->stream>>>(n, S.p, ld, bw.p, 3 * mp, region0, region_w, ypart.p);
     MG_CHECK_LAUNCH(ctx);
-    pass(1, 1, 0, 3 * mp, 1, region0, region_w, nullptr, 0, nullptr, nullptr);
+    k_reduce_cols<<<1, 256, 0, ctx->stream>>>(ypart.p, nb, region_w, Gr0.p);
+    MG_CHECK_LAUNCH(ctx);
+    ar(Gr0.p, (size_t)region_w);
+    k_yaxpy<T><<<grid_for(n * (c_hi - c_lo), 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        n, S.p, ld, 3 * mp, c_lo, c_hi, region0, Gr0.p, ydenom);
+    MG_CHECK_LAUNCH(ctx);
   }
+  DBuf<double> ypart;
 
   // relative pivot floor: ~sqrt of the storage precision's resolution
   static double env_double(const char *name, double dflt) {
