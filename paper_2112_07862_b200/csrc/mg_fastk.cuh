@@ -292,7 +292,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
   unsigned char *after = reinterpret_cast<unsigned char *>(sprec + TK + 4);
   after = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(after) + 15) & ~uintptr_t(15));
   uint64_t *bars = reinterpret_cast<uint64_t *>(after);
-  double *red = reinterpret_cast<double *>(after + 64);     // [kFThreads][8]
+  // [kFThreads][8] column partials, used after the tile loop only: aliases
+  // the (then idle) stage ring, which keeps the shared-memory budget for rows
+  double *red = reinterpret_cast<double *>(smraw);
 
   const int tid = threadIdx.x;
   for (int e = tid; e < mlen; e += kFThreads) sM[e] = Mg[e];

@@ -1285,7 +1285,7 @@ struct Lobpcg {
     const size_t mlen = (size_t)w * mp + (size_t)mp * mp;
     return (size_t)ns * (2 * ((size_t)tk * ld + 16) + tk + 16) * sizeof(T) +
            (mlen + 16 + 4 * (size_t)tk * mp + mp + 4 + tk + 4) * sizeof(T) + 16 + 64 +
-           (size_t)kFThreads * 8 * sizeof(double) + 64;
+           64;  // the column partials alias the stage ring (k_update_resid)
   }
 
   void fast_setup() {
