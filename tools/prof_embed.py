@@ -20,12 +20,27 @@ def main():
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--max-iter", type=int, default=None)
     ap.add_argument("--stats", action="store_true", help="per-class CUDA-event kernel times")
+    ap.add_argument("--morton", action="store_true",
+                    help="experiment: number the points in Morton order of their coordinates "
+                         "and skip the solver's CM reordering (MG_REORDER=0)")
     args = ap.parse_args()
     import torch
     import paper_2112_07862_b200 as mg
     from paper_2112_07862_b200 import core, synthetic
     cfg = synthetic.CONFIGS[args.config]
-    n, ptr, idx, w = synthetic.config_graph(cfg.name, n=args.n)
+    if args.morton:
+        x = synthetic.points(cfg.name, args.n)
+        q = np.minimum((x - x.min(0)) / (np.ptp(x, 0) + 1e-300) * 1024, 1023).astype(np.int64)
+        key = np.zeros(len(x), np.int64)
+        for bit in range(10):
+            for d in range(x.shape[1]):
+                key |= ((q[:, d] >> bit) & 1) << (x.shape[1] * bit + d)
+        x = x[np.argsort(key, kind="stable")]
+        n, ptr, idx, w = synthetic.knn_csr(x, cfg.knn)
+        import os
+        os.environ["MG_REORDER"] = "0"
+    else:
+        n, ptr, idx, w = synthetic.config_graph(cfg.name, n=args.n)
     K = cfg.k
     scfg = mg.SolverConfig(k=K + 1, tol=cfg.tol, max_iter=args.max_iter or cfg.max_iter, seed=42,
                            precision=cfg.precision)
