@@ -251,6 +251,9 @@ def main():
     K = cfg.k
     scfg = mg.SolverConfig(k=K + 1, tol=cfg.tol, max_iter=max_iter, seed=42, precision=prec)
     G = mg.Graph(n, ptr, idx, w)
+    # config 4 is 10 disjoint patches: embed() raises DisconnectedGraphError like
+    # the reference; the config's own harness runs the pair + solve without it
+    connected = cfg.name != "c4"
     zcount = core._stream_size(n, max(K + 1, 8))
     zh = np.random.default_rng(42).standard_normal(zcount)
     dd = torch.device("cuda", device)
@@ -263,9 +266,10 @@ def main():
 
     def embed_dev():
         if comm is None:
-            return core.embed_arrays(n, None, None, None, K, scfg, device_inputs=dev_inputs)
+            return core.embed_arrays(n, None, None, None, K, scfg, device_inputs=dev_inputs,
+                                     check_connected=connected)
         return mgdist.embed_arrays_dist(comm, N.context(device), device, n, None, None, None, K,
-                                        scfg, device_inputs=dev_inputs)
+                                        scfg, device_inputs=dev_inputs, check_connected=connected)
 
     def one_step():
         start = torch.cuda.Event(enable_timing=True)
@@ -313,7 +317,11 @@ def main():
             torch.distributed.barrier()
         t0 = time.perf_counter()
         if comm is None:
-            mg.embed(Gh, K, scfg, require_convergence=False)
+            if connected:
+                mg.embed(Gh, K, scfg, require_convergence=False)
+            else:  # config 4: the reference harness path without the check
+                res_h, b_h, _ = core.embed_arrays(n, ptr, idx, w, K, scfg, check_connected=False)
+                res_h.eigenvectors.cpu(), b_h.cpu()
         else:
             mgdist.embed_dist(comm, Gh, K, scfg, device=device, require_convergence=False)
         torch.cuda.synchronize()
