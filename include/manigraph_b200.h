@@ -212,7 +212,7 @@ int mg_embed_host(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *
 
 /* Gram pair of the fp32 solve on the tensor cores (tcgen05, 3xTF32):
  * GB = S' diag(b) S, GA = S' AS over the first w columns of row-major n x ld
- * fp32 blocks (64 < w <= 128, ld % 4 == 0); outputs w x w row-major fp64.
+ * fp32 blocks (48 < w <= 128, ld % 4 == 0); outputs w x w row-major fp64.
  * Replaces, in one pass over the block, the B-inner products of the
  * reference's _b_mgs_pair (eigensolver.py:127, 143, 145: prefix.T @ (b*rest),
  * U.T @ (b*v), v @ (b*v)) and the Rayleigh-Ritz Gram S.T @ AS

@@ -709,7 +709,7 @@ int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float 
   MG_API_BEGIN(ctx)
   require(n >= 1 && w >= 1 && ld >= w, MG_ERR_INPUT, "bad Gram shape");
   require(gram_tc_supported(w), MG_ERR_INPUT,
-          "tensor-core Gram pair needs 64 < w <= 128 (set MG_TC=1)");
+          "tensor-core Gram pair needs 48 < w <= 128, w % 4 == 0 (and MG_TC != 0)");
   DBuf<double> part;
   gram_pair_tc(ctx, n, ld, w, S, AS, b, GB, GA, part);
   sync(ctx);

@@ -797,13 +797,14 @@ static int tc_pieces() {
 bool gram_tc_supported(int w) {
   const char *e = getenv("MG_TC");
   if (e && e[0] == '0') return false;
-  // converter capacity: (w/4 + 2 ceil-half groups) * 16 rows <= 4 items x 224 threads
-  return w > 64 && w <= 112 && w % 4 == 0;
+  // v2 (mg_tc2.cu, the default) covers 48 < w <= 128; below that the CUDA-core
+  // k_gram2 is faster (the per-tile pipeline cost of v2 dominates small tiles).
+  // v1 (MG_TC_V=1 / MG_TC_PIECES=3): converter capacity limits it to 64 < w <= 112.
+  return w > 48 && w <= 128 && w % 4 == 0;
 }
 
 void gram_pair_tc(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const float *AS,
                   const float *b, double *GB, double *GA, DBuf<double> &part) {
-  require(w >= 4 && w <= 112 && w % 4 == 0, MG_ERR_INTERNAL, "tc Gram: bad width");
   require(ld % 4 == 0, MG_ERR_INTERNAL, "tc Gram: row stride must be a multiple of 4");
   const int NS = tc_pieces();
   {
@@ -813,6 +814,7 @@ void gram_pair_tc(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const f
       return;
     }
   }
+  require(w > 64 && w <= 112 && w % 4 == 0, MG_ERR_INTERNAL, "tc Gram v1: needs 64 < w <= 112");
   const int TK = NS == 3 ? TcCfg<3>::TK : TcCfg<2>::TK;
   const int64_t ntiles = (n + TK - 1) / TK;
   const int npairs = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ctx->num_sms / 2));

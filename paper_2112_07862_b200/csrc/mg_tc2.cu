@@ -435,7 +435,7 @@ CUtensorMap make_map_1d(const float *base, int64_t n) {
 }  // namespace
 
 bool gram_tc2_supported(int w, int ld) {
-  return w > 64 && w <= 128 && ld % 4 == 0 && w % 4 == 0;
+  return w > 32 && w <= 128 && ld % 4 == 0 && w % 4 == 0;
 }
 
 void gram_pair_tc2(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const float *AS,
