@@ -44,7 +44,8 @@ typedef enum mg_status {
   MG_ERR_CUDA = 4,
   MG_ERR_NCCL = 5,
   MG_ERR_NOMEM = 6,
-  MG_ERR_INTERNAL = 7
+  MG_ERR_INTERNAL = 7,
+  MG_ERR_PARSE = 8 /* -> ParseError (errors.py:14-20); see mg_load_edge_list_count */
 } mg_status;
 
 typedef struct mg_ctx mg_ctx;
@@ -219,6 +220,28 @@ int mg_embed_host(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *
  * (eigensolver.py:251), at the K = 16..32 block widths. */
 int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float *S,
                      const float *AS, const float *b, double *GB, double *GA);
+
+/* ---------------------------------------- text I/O -------
+ * Host arrays, host files; the same bytes as the reference writers and the
+ * same values / errors as its readers.  threads <= 0: all host cores. */
+/* save_embedding_csv (embedding.py:131-140): "node,c1,...,cK" + rows "i,v,..."
+ * with format(v, '.17g'); P row-major n x k */
+int mg_save_embedding_csv(const char *path, int64_t n, int32_t k, const double *P,
+                          int32_t threads);
+/* load_embedding_csv (embedding.py:143-166): _dims returns (n, k); the fill
+ * call writes P (row-major n x k, rows in node-id order) */
+int mg_load_embedding_csv_dims(const char *path, int64_t *n, int32_t *k);
+int mg_load_embedding_csv(const char *path, int64_t n, int32_t k, double *P, int32_t threads);
+/* save_edge_list (graph.py:188-194): "i\tj\tw" for i < j, 17-digit weights */
+int mg_save_edge_list(const char *path, int64_t n, const int64_t *indptr, const int64_t *indices,
+                      const double *weights, int32_t threads);
+/* load_edge_list (graph.py:147-185) -> Graph.from_edges CSR.  _count parses
+ * and keeps the result for the calling thread (n, nnz; on MG_ERR_PARSE the
+ * 1-based line in *err_line); _fill copies it out (indptr n+1, indices and
+ * weights nnz) and releases it. */
+int mg_load_edge_list_count(const char *path, int32_t threads, int64_t *n, int64_t *nnz,
+                            int64_t *err_line);
+int mg_load_edge_list_fill(int64_t *indptr, int64_t *indices, double *weights);
 
 /* --------------------------------------- kNN graph -------
  * knn_graph (graph.py:281-315): symmetrized k-nearest-neighbour graph of the

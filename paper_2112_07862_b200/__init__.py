@@ -36,6 +36,12 @@ from .core import (  # noqa: F401
 )
 from .clustering import kmeans, normalize_rows  # noqa: F401
 from .knn import knn_graph  # noqa: F401
+from .textio import (  # noqa: F401
+    load_edge_list,
+    load_embedding_csv,
+    save_edge_list,
+    save_embedding_csv,
+)
 from .errors import (  # noqa: F401
     ConvergenceError,
     DisconnectedGraphError,

@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(HERE, "_native", "libmgb200.so")
 
 MG_OK, MG_ERR_INPUT, MG_ERR_DISCONNECTED, MG_ERR_NOT_CONVERGED = 0, 1, 2, 3
 MG_ERR_CUDA, MG_ERR_NCCL, MG_ERR_NOMEM, MG_ERR_INTERNAL = 4, 5, 6, 7
+MG_ERR_PARSE = 8
 
 i64 = C.c_int64
 i32 = C.c_int32
@@ -83,6 +84,12 @@ SIGNATURES = {
     "mg_gram_pair_f32": [vp, i64, i32, i32, vp, vp, vp, vp, vp],
     "mg_kmeans": [vp, i64, i32, vp, i32, i32, C.c_uint64, vp, P_f64],
     "mg_knn_graph_count": [vp, i64, i32, vp, i32, i32, vp, P_i64],
+    "mg_save_embedding_csv": [C.c_char_p, i64, i32, vp, i32],
+    "mg_load_embedding_csv_dims": [C.c_char_p, P_i64, P_i32],
+    "mg_load_embedding_csv": [C.c_char_p, i64, i32, vp, i32],
+    "mg_save_edge_list": [C.c_char_p, i64, vp, vp, vp, i32],
+    "mg_load_edge_list_count": [C.c_char_p, i32, P_i64, P_i64, P_i64],
+    "mg_load_edge_list_fill": [vp, vp, vp],
     "mg_knn_graph_fill": [vp, i64, i32, vp, i32, i32, vp, vp],
     "mg_normalize_rows": [vp, i64, i32, vp, vp],
     # multi-GPU (row-partitioned solve)

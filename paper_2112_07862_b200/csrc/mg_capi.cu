@@ -11,6 +11,7 @@
 #include "mg_tc.cuh"
 #include "mg_kmeans.cuh"
 #include "mg_knn.cuh"
+#include "mg_io.cuh"
 #include "mg_graph.cuh"
 #include "mg_small.cuh"
 
@@ -713,6 +714,71 @@ int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float 
   DBuf<double> part;
   gram_pair_tc(ctx, n, ld, w, S, AS, b, GB, GA, part);
   sync(ctx);
+  MG_API_END
+}
+
+int mg_save_embedding_csv(const char *path, int64_t n, int32_t k, const double *P,
+                          int32_t threads) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(path != nullptr, MG_ERR_INPUT, "path is NULL");
+  save_embedding_csv(path, n, k, P, threads);
+  MG_API_END
+}
+
+int mg_load_embedding_csv_dims(const char *path, int64_t *n, int32_t *k) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(path != nullptr && n != nullptr && k != nullptr, MG_ERR_INPUT, "NULL argument");
+  int kk = 0;
+  load_embedding_csv(path, n, &kk, nullptr, 1);
+  *k = kk;
+  MG_API_END
+}
+
+int mg_load_embedding_csv(const char *path, int64_t n, int32_t k, double *P, int32_t threads) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(path != nullptr && P != nullptr, MG_ERR_INPUT, "NULL argument");
+  int64_t n2 = 0;
+  int k2 = 0;
+  load_embedding_csv(path, &n2, &k2, nullptr, 1);
+  require(n2 == n && k2 == k, MG_ERR_INPUT, "embedding dimensions changed between calls");
+  load_embedding_csv(path, &n2, &k2, P, threads);
+  MG_API_END
+}
+
+int mg_save_edge_list(const char *path, int64_t n, const int64_t *indptr, const int64_t *indices,
+                      const double *weights, int32_t threads) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(path != nullptr && indptr != nullptr, MG_ERR_INPUT, "NULL argument");
+  save_edge_list(path, n, indptr, indices, weights, threads);
+  MG_API_END
+}
+
+static thread_local mg::EdgeListResult tl_edges;
+
+int mg_load_edge_list_count(const char *path, int32_t threads, int64_t *n, int64_t *nnz,
+                            int64_t *err_line) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(path != nullptr && n != nullptr && nnz != nullptr, MG_ERR_INPUT, "NULL argument");
+  tl_edges = mg::EdgeListResult();
+  try {
+    load_edge_list(path, threads, tl_edges);
+  } catch (...) {
+    if (err_line) *err_line = tl_edges.err_line;
+    throw;
+  }
+  *n = tl_edges.n;
+  *nnz = (int64_t)tl_edges.indices.size();
+  MG_API_END
+}
+
+int mg_load_edge_list_fill(int64_t *indptr, int64_t *indices, double *weights) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(indptr != nullptr && !tl_edges.indptr.empty(), MG_ERR_INPUT,
+          "mg_load_edge_list_fill without a successful mg_load_edge_list_count");
+  std::memcpy(indptr, tl_edges.indptr.data(), tl_edges.indptr.size() * sizeof(int64_t));
+  std::memcpy(indices, tl_edges.indices.data(), tl_edges.indices.size() * sizeof(int64_t));
+  std::memcpy(weights, tl_edges.weights.data(), tl_edges.weights.size() * sizeof(double));
+  tl_edges = mg::EdgeListResult();
   MG_API_END
 }
 
