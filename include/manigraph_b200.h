@@ -221,6 +221,13 @@ int mg_embed_host(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *
 int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float *S,
                      const float *AS, const float *b, double *GB, double *GA);
 
+/* numpy's Generator(PCG64).standard_normal stream, bit for bit, on the device:
+ * the reference's initial block (eigensolver.py:177-178, 189) is the first
+ * n*m values of default_rng(seed).standard_normal.  (state, inc) are the 128-bit
+ * halves of default_rng(seed).bit_generator.state['state']; out: device double[count]. */
+int mg_normal_stream(mg_ctx *ctx, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                     uint64_t inc_lo, int64_t count, double *out);
+
 /* ---------------------------------------- text I/O -------
  * Host arrays, host files; the same bytes as the reference writers and the
  * same values / errors as its readers.  threads <= 0: all host cores. */

@@ -84,6 +84,7 @@ SIGNATURES = {
     "mg_gram_pair_f32": [vp, i64, i32, i32, vp, vp, vp, vp, vp],
     "mg_kmeans": [vp, i64, i32, vp, i32, i32, C.c_uint64, vp, P_f64],
     "mg_knn_graph_count": [vp, i64, i32, vp, i32, i32, vp, P_i64],
+    "mg_normal_stream": [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, i64, vp],
     "mg_save_embedding_csv": [C.c_char_p, i64, i32, vp, i32],
     "mg_load_embedding_csv_dims": [C.c_char_p, P_i64, P_i32],
     "mg_load_embedding_csv": [C.c_char_p, i64, i32, vp, i32],

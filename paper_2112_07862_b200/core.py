@@ -87,9 +87,21 @@ def _call(name, *args):
 
 
 def _normals(seed: int, count: int):
-    """numpy PCG64(seed).standard_normal stream (eigensolver.py:177-178, 189)."""
-    z = np.random.default_rng(seed).standard_normal(int(count))
-    return _dev(z, _t().float64), int(count)
+    """numpy PCG64(seed).standard_normal stream (eigensolver.py:177-178, 189),
+    generated on the device bit for bit (csrc/mg_rng.cu); MG_HOST_NORMALS=1 uses
+    numpy on the host instead."""
+    import os
+    count = int(count)
+    if os.environ.get("MG_HOST_NORMALS", "0") == "1":
+        z = np.random.default_rng(seed).standard_normal(count)
+        return _dev(z, _t().float64), count
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    m64 = (1 << 64) - 1
+    s, inc = int(st["state"]), int(st["inc"])
+    out = _empty(count, _t().float64)
+    _call("mg_normal_stream", _ctx(), C.c_uint64(s >> 64), C.c_uint64(s & m64),
+          C.c_uint64(inc >> 64), C.c_uint64(inc & m64), count, _ptr(out))
+    return out[:count] if count else out, count
 
 
 # ------------------------------------------------------------------- types ---

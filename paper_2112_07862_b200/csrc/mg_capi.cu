@@ -12,6 +12,7 @@
 #include "mg_kmeans.cuh"
 #include "mg_knn.cuh"
 #include "mg_io.cuh"
+#include "mg_rng.cuh"
 #include "mg_graph.cuh"
 #include "mg_small.cuh"
 
@@ -714,6 +715,14 @@ int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float 
   DBuf<double> part;
   gram_pair_tc(ctx, n, ld, w, S, AS, b, GB, GA, part);
   sync(ctx);
+  MG_API_END
+}
+
+int mg_normal_stream(mg_ctx *ctx, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                     uint64_t inc_lo, int64_t count, double *out) {
+  MG_API_BEGIN(ctx)
+  require(out != nullptr || count == 0, MG_ERR_INPUT, "out is NULL");
+  normal_stream(ctx, state_hi, state_lo, inc_hi, inc_lo, count, out);
   MG_API_END
 }
 
