@@ -85,6 +85,8 @@ SIGNATURES = {
     "mg_kmeans": [vp, i64, i32, vp, i32, i32, C.c_uint64, vp, P_f64],
     "mg_knn_graph_count": [vp, i64, i32, vp, i32, i32, vp, P_i64],
     "mg_normal_stream": [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, i64, vp],
+    "mg_copy_d2h": [vp, vp, vp, i64],
+    "mg_copy_h2d": [vp, vp, vp, i64],
     "mg_save_embedding_csv": [C.c_char_p, i64, i32, vp, i32],
     "mg_load_embedding_csv_dims": [C.c_char_p, P_i64, P_i32],
     "mg_load_embedding_csv": [C.c_char_p, i64, i32, vp, i32],

@@ -48,7 +48,26 @@ def _dev(a, dtype):
         return a.to(device="cuda", dtype=dtype).contiguous()
     npdt = {torch.int64: np.int64, torch.float64: np.float64}[dtype]
     arr = np.ascontiguousarray(np.asarray(a, dtype=npdt))
-    return torch.from_numpy(arr).to("cuda")
+    if arr.nbytes <= (8 << 20):
+        return torch.from_numpy(arr).to("cuda")
+    out = torch.empty(arr.shape, dtype=dtype, device="cuda")
+    _sync()  # the allocation is on torch's stream; the copy runs on the library's
+    N.call("mg_copy_h2d", N.context(0), _ptr(out), arr.ctypes.data_as(C.c_void_p), arr.nbytes)
+    return out
+
+
+def _host(t):
+    """CUDA tensor -> numpy array (pipelined pinned-stage copy for large results)."""
+    torch = _t()
+    t = t.contiguous()
+    if t.numel() * t.element_size() <= (8 << 20):
+        return t.cpu().numpy()
+    npdt = {torch.int64: np.int64, torch.int32: np.int32, torch.float64: np.float64,
+            torch.float32: np.float32}[t.dtype]
+    out = np.empty(tuple(t.shape), dtype=npdt)
+    _sync()
+    N.call("mg_copy_d2h", N.context(0), out.ctypes.data_as(C.c_void_p), _ptr(t), out.nbytes)
+    return out
 
 
 def _ptr(t):
@@ -382,7 +401,7 @@ def connected_components(g):
     cnt = C.c_int64(0)
     _sync()
     _call("mg_components", _ctx(), g.n, _ptr(p), _ptr(i), _ptr(labels), C.byref(cnt))
-    return int(cnt.value), labels[:g.n].cpu().numpy()
+    return int(cnt.value), _host(labels[:g.n])
 
 
 def spmm(a, X):
@@ -398,7 +417,7 @@ def spmm(a, X):
     y = _empty(a.n * k, torch.float64)
     _sync()
     _call("mg_spmm", _ctx(), a.n, _ptr(p), _ptr(i), _ptr(d), _ptr(x), k, _ptr(y))
-    return y[:a.n * k].view(a.n, k).cpu().numpy()
+    return _host(y[:a.n * k].view(a.n, k))
 
 
 def laplacian(g) -> SparseSymMatrix:
@@ -410,8 +429,8 @@ def laplacian(g) -> SparseSymMatrix:
     op, oi, od = _empty(g.n + 1, torch.int64), _empty(nnz, torch.int64), _empty(nnz, torch.float64)
     _sync()
     _call("mg_laplacian", _ctx(), g.n, _ptr(p), _ptr(i), _ptr(w), _ptr(op), _ptr(oi), _ptr(od))
-    m = SparseSymMatrix(g.n, op[:g.n + 1].cpu().numpy(), oi[:nnz].cpu().numpy(),
-                        od[:nnz].cpu().numpy())
+    m = SparseSymMatrix(g.n, _host(op[:g.n + 1]), _host(oi[:nnz]),
+                        _host(od[:nnz]))
     object.__setattr__(m, "_dcache", (op[:g.n + 1], oi[:nnz], od[:nnz]))
     return m
 
@@ -427,7 +446,7 @@ def two_hop_sets(g) -> TwoHopSets:
     _call("mg_two_hop_count", _ctx(), g.n, _ptr(p), _ptr(i), _ptr(tp), C.byref(nnz))
     ti = _empty(nnz.value, torch.int64)
     _call("mg_two_hop_fill", _ctx(), g.n, _ptr(p), _ptr(i), _ptr(tp), _ptr(ti))
-    t = TwoHopSets(n=g.n, indptr=tp[:g.n + 1].cpu().numpy(), indices=ti[:nnz.value].cpu().numpy())
+    t = TwoHopSets(n=g.n, indptr=_host(tp[:g.n + 1]), indices=_host(ti[:nnz.value]))
     object.__setattr__(t, "_dcache", (tp[:g.n + 1], ti[:nnz.value]))
     return t
 
@@ -448,7 +467,7 @@ def two_hop_laplacian(t, literal_diagonal: bool = False) -> SparseSymMatrix:
     _call("mg_two_hop_laplacian_fill", _ctx(), n, _ptr(tp), _ptr(ti), int(bool(literal_diagonal)),
           _ptr(qp), _ptr(qi), _ptr(qd))
     k = nnz.value
-    m = SparseSymMatrix(n, qp[:n + 1].cpu().numpy(), qi[:k].cpu().numpy(), qd[:k].cpu().numpy())
+    m = SparseSymMatrix(n, _host(qp[:n + 1]), _host(qi[:k]), _host(qd[:k]))
     object.__setattr__(m, "_dcache", (qp[:n + 1], qi[:k], qd[:k]))
     return m
 
@@ -513,7 +532,7 @@ def assemble_operator(l, q, mu: float, epsilon: float) -> SparseSymMatrix:
     ai, ad = _empty(k, torch.int64), _empty(k, torch.float64)
     _call("mg_assemble_fill", _ctx(), n, _ptr(lp), _ptr(li), _ptr(ld), _ptr(qp), _ptr(qi),
           _ptr(qd), float(mu), float(epsilon), _ptr(ap), _ptr(ai), _ptr(ad))
-    m = SparseSymMatrix(n, ap[:n + 1].cpu().numpy(), ai[:k].cpu().numpy(), ad[:k].cpu().numpy())
+    m = SparseSymMatrix(n, _host(ap[:n + 1]), _host(ai[:k]), _host(ad[:k]))
     object.__setattr__(m, "_dcache", (ap[:n + 1], ai[:k], ad[:k]))
     return m
 
@@ -529,7 +548,7 @@ def degree_balancing(a) -> DiagonalScaling:
     _sync()
     _call("mg_degree_balancing", _ctx(), a.n, _ptr(p), _ptr(i), _ptr(d), _ptr(b), C.byref(g),
           C.byref(bad))
-    return DiagonalScaling(b=b[:a.n].cpu().numpy(), generalized_degree=float(g.value))
+    return DiagonalScaling(b=_host(b[:a.n]), generalized_degree=float(g.value))
 
 
 def build_operator_pair(g, literal_diagonal: bool = False, solver_seed: int = 42) -> OperatorPair:
@@ -595,7 +614,7 @@ def lobpcg_smallest(a, b, cfg: SolverConfig, deflate=None) -> EigenResult:
                 count *= 8
                 continue
             _raise_native(e)
-    return EigenResult(eigenvalues=ev.copy(), eigenvectors=vecs[:n * k].view(n, k).cpu().numpy(),
+    return EigenResult(eigenvalues=ev.copy(), eigenvectors=_host(vecs[:n * k].view(n, k)),
                        iterations=int(out.iterations), residual_norms=rn.copy(),
                        converged=cv.astype(bool), ritz_sum_history=list(hist[:out.history_len]))
 
@@ -715,11 +734,11 @@ def embed(g, k: int, cfg: SolverConfig | None = None, literal_diagonal: bool = F
                 z, nz = _normals(cfg.seed, nz * 8)
                 continue
             raise
-    res.eigenvectors = res.eigenvectors.cpu().numpy()
+    res.eigenvectors = _host(res.eigenvectors)
     if require_convergence:
         require_converged(res, "embedding eigensolve")
     return Embedding(P=res.eigenvectors[:, 1:], method="proposed",
-                     eigenvalues=res.eigenvalues[1:], b=b.cpu().numpy(),
+                     eigenvalues=res.eigenvalues[1:], b=_host(b),
                      diagnostics=_diag_dict(dg, res))
 
 

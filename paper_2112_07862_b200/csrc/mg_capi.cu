@@ -470,6 +470,7 @@ int mg_ctx_destroy(mg_ctx *ctx) {
   cudaStreamSynchronize(ctx->stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  free_stages(ctx);
   for (auto &r : ctx->prof) {
     cudaEventDestroy(r.start);
     cudaEventDestroy(r.stop);
@@ -715,6 +716,20 @@ int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float 
   DBuf<double> part;
   gram_pair_tc(ctx, n, ld, w, S, AS, b, GB, GA, part);
   sync(ctx);
+  MG_API_END
+}
+
+int mg_copy_d2h(mg_ctx *ctx, void *host, const void *dev, int64_t bytes) {
+  MG_API_BEGIN(ctx)
+  require(bytes >= 0 && (bytes == 0 || (host && dev)), MG_ERR_INPUT, "bad copy arguments");
+  d2h_sync(ctx, host, dev, (size_t)bytes);
+  MG_API_END
+}
+
+int mg_copy_h2d(mg_ctx *ctx, void *dev, const void *host, int64_t bytes) {
+  MG_API_BEGIN(ctx)
+  require(bytes >= 0 && (bytes == 0 || (host && dev)), MG_ERR_INPUT, "bad copy arguments");
+  h2d(ctx, dev, host, (size_t)bytes);
   MG_API_END
 }
 

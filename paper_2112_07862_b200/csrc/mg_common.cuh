@@ -62,6 +62,8 @@ struct mg_ctx {
   int64_t launches = 0;
   void *pinned = nullptr;       // small pinned staging buffer for D2H scalars
   size_t pinned_bytes = 0;
+  void *stage[2] = {nullptr, nullptr};  // pinned ring for large host <-> device copies
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   int profiling = 0;            // record CUDA events around hot kernels
   std::vector<mg_prof_rec> prof;
   std::vector<cudaEvent_t> event_pool;
@@ -121,6 +123,12 @@ struct ProfScope {
   ProfScope(mg_ctx *c, int cls, double bytes);
   ~ProfScope();
 };
+
+// Large host <-> device copies (pageable host memory): pipelined through two
+// pinned 64 MB stages, the host-side memcpy split over threads.
+void d2h_large(mg_ctx *ctx, void *host, const void *dev, size_t bytes);
+void h2d_large(mg_ctx *ctx, void *dev, const void *host, size_t bytes);
+void free_stages(mg_ctx *ctx);
 
 // Copy device -> host through the context's pinned staging area and wait.
 void d2h_sync(mg_ctx *ctx, void *host, const void *dev, size_t bytes);

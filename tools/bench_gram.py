@@ -9,7 +9,7 @@ for n in [int(x) for x in os.environ.get("NS", "2000000 20000000").split()]:
     AS = torch.randn(n, ld, device='cuda') / 1000
     b = torch.rand(n, device='cuda') + 0.5
     GB = torch.zeros(w*w, dtype=torch.float64, device='cuda'); GA = torch.zeros_like(GB)
-    for v in os.environ.get('VS', '1 2').split():
+    for v in os.environ.get('VS', '1 2').split():  # MG_TC_V value: 1 = v1, 2 = v2, else v4
         os.environ['MG_TC_V'] = v
         f = lambda: N.call("mg_gram_pair_f32", N.context(0), n, ld, w, C.c_void_p(S.data_ptr()), C.c_void_p(AS.data_ptr()),
                    C.c_void_p(b.data_ptr()), C.c_void_p(GB.data_ptr()), C.c_void_p(GA.data_ptr()))
