@@ -512,6 +512,213 @@ __global__ void __launch_bounds__(kFThreads, 1)
   }
 }
 
+// ------------------------------------------------------------ k_update_ws ---
+// fp32 k_update_resid with warp specialisation: warps 0-7 form the P / X
+// register-blocked products of tile t while warps 8-11 run the residual, W,
+// column norms and the global write-back of tile t-1 (double-buffered output
+// tiles).  In k_update_resid those phases alternate behind __syncthreads and
+// the FMA pipes idle during the write-back (~30 % of the samples, ncu).
+// Barriers: full[s] (TMA), rdy[o] (8 FMA warps -> output tile o complete),
+// fre[o] (4 store warps -> output tile o consumed, stage refilled).
+constexpr int kWsF = 256, kWsS = 128;
+
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__host__ __device__ inline size_t upd_ws_bytes(int tk, int ld, int w, int mp) {
+  const size_t tile = (size_t)tk * ld + 16;
+  return (size_t)3 * (2 * tile + tk + 16) * 4 + ((size_t)w * mp + (size_t)mp * mp + 16) * 4 +
+         (size_t)8 * tk * mp * 4 + (size_t)(mp + 4) * 4 + 256;
+}
+
+template <int RT>
+__global__ void __launch_bounds__(kWsF + kWsS, 1)
+    k_update_ws(float *__restrict__ S, float *__restrict__ AS, const float *__restrict__ b,
+                const float *__restrict__ prec, const float *__restrict__ Mg,
+                const double *__restrict__ theta, UpdArgs a) {
+  if (*a.skip) return;
+  constexpr int NS = 3;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int ld = a.ld, w = a.w, mp = a.mp, TK = a.tk;
+  const size_t tile_elems = (size_t)TK * ld + 16;
+  float *ring = reinterpret_cast<float *>(smraw);
+  auto stS = [&](int s) { return ring + (size_t)s * (2 * tile_elems + TK + 16); };
+  auto stA = [&](int s) { return stS(s) + tile_elems; };
+  auto stB = [&](int s) { return stS(s) + 2 * tile_elems; };
+  float *sM = ring + (size_t)NS * (2 * tile_elems + TK + 16);
+  const int mlen = w * mp + mp * mp;
+  float *obuf = sM + mlen + 16;  // [2][4][TK][mp]: P_S, P_A, X_S, X_A
+  auto oP = [&](int o, int mat) { return obuf + ((size_t)o * 4 + mat) * TK * mp; };
+  auto oX = [&](int o, int mat) { return obuf + ((size_t)o * 4 + 2 + mat) * TK * mp; };
+  float *sth = obuf + (size_t)8 * TK * mp;
+  unsigned char *after = reinterpret_cast<unsigned char *>(sth + mp + 4);
+  after = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(after) + 15) & ~uintptr_t(15));
+  uint64_t *full = reinterpret_cast<uint64_t *>(after);
+  uint64_t *rdy = full + NS, *fre = rdy + 2;
+  double *red = reinterpret_cast<double *>(smraw);  // after the loop (aliases the ring)
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < mlen; e += blockDim.x) sM[e] = Mg[e];
+  for (int e = tid; e < mp; e += blockDim.x) sth[e] = e < a.m ? (float)theta[e] : 0.f;
+  const int64_t ntiles = (a.n + TK - 1) / TK;
+  const int64_t t_begin = ntiles * blockIdx.x / gridDim.x;
+  const int64_t t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
+  if (tid == 0) {
+    for (int q = 0; q < NS; ++q) mbar_init(&full[q], 1);
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&rdy[q], kWsF / 32);
+      mbar_init(&fre[q], kWsS / 32);
+    }
+    fence_proxy_async();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int q = 0; q < NS && t_begin + q < t_end; ++q)
+      issue_tile<float>(S, AS, b, a.n, ld, TK, t_begin + q, stS(q), stA(q), stB(q), &full[q]);
+
+  const int C4 = mp / 4, R4 = kWsS / C4;
+  double sr4[4] = {0.0, 0.0, 0.0, 0.0}, sx4[4] = {0.0, 0.0, 0.0, 0.0};
+  if (tid < kWsF) {
+    // ------------------------------------------------------ FMA warps
+    const float *Zp = sM, *Yx = sM + w * mp;
+    const int cb = (mp + 3) / 4, nblk = (TK / RT) * cb;
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      const int lt = (int)(t - t_begin), s = lt % NS, o = lt & 1;
+      mbar_wait(&full[s], (uint32_t)((lt / NS) & 1));
+      mbar_wait(&fre[o], (uint32_t)(((lt >> 1) & 1) ^ 1));
+      for (int phase = 0; phase < 2; ++phase) {
+        const int K = phase == 0 ? w : mp;
+        const float *Bm = phase == 0 ? Zp : Yx;
+        const int RS = TK / RT;
+        const int nrb = TK / RT, cbA = min(cb, 8), cbB = cb - cbA;
+        const int nJA = 2 * nrb * cbA;
+        for (int job = tid; job < 2 * nblk; job += kWsF) {
+          int mat, rb, c0;
+          if (job < nJA) {
+            mat = job / (nrb * cbA);
+            const int rem = job - mat * nrb * cbA;
+            rb = rem / cbA;
+            c0 = (rem - rb * cbA) * 4;
+          } else {
+            const int j2 = job - nJA;
+            mat = j2 / (nrb * cbB);
+            const int rem = j2 - mat * nrb * cbB;
+            rb = rem / cbB;
+            c0 = (8 + rem - rb * cbB) * 4;
+          }
+          const float *src = (mat ? stA(s) : stS(s)) + rb * ld;
+          float acc[RT][4];
+          if (phase == 0) {
+#pragma unroll
+            for (int x = 0; x < RT; ++x)
+#pragma unroll
+              for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
+          } else {
+            const float *pn = oP(o, mat) + rb * mp + c0;
+#pragma unroll
+            for (int x = 0; x < RT; ++x) {
+              const float4 v = *reinterpret_cast<const float4 *>(pn + x * RS * mp);
+              acc[x][0] = v.x;
+              acc[x][1] = v.y;
+              acc[x][2] = v.z;
+              acc[x][3] = v.w;
+            }
+          }
+#pragma unroll 3
+          for (int k = 0; k < K; k += 4) {
+            float4 bb[4];
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              bb[kk] = *reinterpret_cast<const float4 *>(Bm + (k + kk) * mp + c0);
+#pragma unroll
+            for (int x = 0; x < RT; ++x) {
+              const float4 av = *reinterpret_cast<const float4 *>(src + x * RS * ld + k);
+              const float aa[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                acc[x][0] += aa[kk] * bb[kk].x;
+                acc[x][1] += aa[kk] * bb[kk].y;
+                acc[x][2] += aa[kk] * bb[kk].z;
+                acc[x][3] += aa[kk] * bb[kk].w;
+              }
+            }
+          }
+          float *dst = (phase == 0 ? oP(o, mat) : oX(o, mat)) + rb * mp + c0;
+#pragma unroll
+          for (int x = 0; x < RT; ++x)
+            *reinterpret_cast<float4 *>(dst + x * RS * mp) =
+                make_float4(acc[x][0], acc[x][1], acc[x][2], acc[x][3]);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kWsF) : "memory");  // FMA warps only
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&rdy[o]);  // release: tile o's products visible
+    }
+  } else {
+    // ---------------------------------------------------- store warps
+    const int st = tid - kWsF;
+    const int rc4 = st % C4, rrow4 = st / C4;
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      const int lt = (int)(t - t_begin), s = lt % NS, o = lt & 1;
+      mbar_wait(&rdy[o], (uint32_t)((lt >> 1) & 1));
+      const int64_t r0 = t * TK;
+      const int nr = (int)min((int64_t)TK, a.n - r0);
+      for (int rr = rrow4; rr < nr && rrow4 < R4; rr += R4) {
+        const float4 x = *reinterpret_cast<const float4 *>(oX(o, 0) + rr * mp + 4 * rc4);
+        const float4 ax = *reinterpret_cast<const float4 *>(oX(o, 1) + rr * mp + 4 * rc4);
+        const float xs[4] = {x.x, x.y, x.z, x.w}, axs[4] = {ax.x, ax.y, ax.z, ax.w};
+        const float br = stB(s)[rr], pr = prec ? prec[r0 + rr] : 1.f;
+        float wv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          wv[q] = 0.f;
+          if (4 * rc4 + q < a.m) {
+            const float r = axs[q] - br * xs[q] * sth[4 * rc4 + q];
+            sr4[q] += (double)r * (double)r;
+            sx4[q] += (double)xs[q] * (double)xs[q];
+            wv[q] = pr * r;
+          }
+        }
+        const float4 w4 = make_float4(wv[0], wv[1], wv[2], wv[3]);
+        float *srow = S + (r0 + rr) * ld + 4 * rc4;
+        float *arow = AS + (r0 + rr) * ld + 4 * rc4;
+        *reinterpret_cast<float4 *>(srow) = x;
+        *reinterpret_cast<float4 *>(srow + mp) =
+            *reinterpret_cast<const float4 *>(oP(o, 0) + rr * mp + 4 * rc4);
+        *reinterpret_cast<float4 *>(srow + 2 * mp) = w4;
+        reinterpret_cast<float4 *>(reinterpret_cast<float *>(a.wc) + (r0 + rr) * mp)[rc4] = w4;
+        *reinterpret_cast<float4 *>(arow) = ax;
+        *reinterpret_cast<float4 *>(arow + mp) =
+            *reinterpret_cast<const float4 *>(oP(o, 1) + rr * mp + 4 * rc4);
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(kWsS) : "memory");  // store warps only
+      if (st == 0 && t + NS < t_end) {  // stage s fully consumed: refill it
+        fence_proxy_async();
+        issue_tile<float>(S, AS, b, a.n, ld, TK, t + NS, stS(s), stA(s), stB(s), &full[s]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&fre[o]);
+    }
+  }
+  __syncthreads();
+  if (tid >= kWsF) {
+    const int st = tid - kWsF;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      red[st * 8 + q] = (st / C4 < R4) ? sr4[q] : 0.0;
+      red[st * 8 + 4 + q] = (st / C4 < R4) ? sx4[q] : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < 2 * mp; c += blockDim.x) {
+    const int col = c % mp, which = c / mp;
+    double s2 = 0.0;
+    for (int q = 0; q < R4; ++q) s2 += red[(q * C4 + col / 4) * 8 + 4 * which + (col & 3)];
+    a.part[(size_t)blockIdx.x * 2 * mp + c] = s2;
+  }
+}
+
 // ---------------------------------------------------------- k_ctrl_fast ---
 // Small-matrix LOBPCG step for a prefix iteration.  G_B / G_A are w x w over
 // physical columns [0, w) = [X | P | W].  Logical basis: X (m trusted

@@ -1275,6 +1275,9 @@ struct Lobpcg {
   int64_t fast_steps = 0, fast_fallbacks = 0;
 
   int tk_gram = 32, ns_gram = 3, tk_upd = 32, rt_upd = 8;
+  bool upd_ws = false;
+  int tk_ws = 0;
+  size_t ws_smem = 0;
 
   size_t gram2_bytes(int tk, int ns) const {
     return (size_t)ns * (2 * ((size_t)tk * ld + 16) + tk + 16) * sizeof(T) + 16 + 64 +
@@ -1324,6 +1327,21 @@ struct Lobpcg {
     if (const char *e = getenv("MG_UPD_RT")) rt_upd = atoi(e);
     gram2_smem = gram2_bytes(tk_gram, ns_gram);
     upd_smem = upd_bytes(tk_upd, 3);
+    // fp32: warp-specialised update (k_update_ws) when its double-buffered
+    // output tiles fit with >= 32-row tiles
+    upd_ws = false;
+    if (sizeof(T) == 4 && env_double("MG_UPD_WS", 1) != 0 && mp % 4 == 0) {
+      for (int tk = 64; tk >= 32; tk -= 4)
+        if (upd_ws_bytes(tk, ld, 3 * mp, mp) <= budget && (tk / 4) * ((mp + 3) / 4) * 2 >= 128) {
+          upd_ws = true;
+          tk_ws = tk;
+          ws_smem = upd_ws_bytes(tk, ld, 3 * mp, mp);
+          break;
+        }
+      if (upd_ws)
+        MG_CUDA(cudaFuncSetAttribute(k_update_ws<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)ws_smem));
+    }
     int smax = m + 2 * m;
     size_t need = (size_t)2 * std::max(smax * smax, 4 * m * m) * sizeof(double);
     fast_global = need > 190 * 1024;
@@ -1473,6 +1491,17 @@ struct Lobpcg {
           nblk_upd = update_tc(ctx, n, ld, w, m, mp, (float *)S.p, (float *)AS.p,
                                (const float *)bw.p, (const float *)pr, (const float *)M.p,
                                theta.p, status.p + 5, colpart.p, (float *)Wc.p);
+          goto upd_done;
+        }
+      }
+      if constexpr (sizeof(T) == 4) {
+        if (upd_ws) {
+          UpdArgs uw = ua;
+          uw.tk = tk_ws;
+          k_update_ws<4><<<grid_upd, kWsF + kWsS, ws_smem, ctx->stream>>>(
+              (float *)S.p, (float *)AS.p, (const float *)bw.p, (const float *)pr,
+              (const float *)M.p, theta.p, uw);
+          MG_CHECK_LAUNCH(ctx);
           goto upd_done;
         }
       }
