@@ -625,16 +625,27 @@ __global__ void __launch_bounds__(kWsF + kWsS, 1)
               acc[x][3] = v.w;
             }
           }
-#pragma unroll 3
+          // register double buffering: the next k-quad's shared-memory loads
+          // are in flight while this quad's FMAs issue (short-scoreboard stalls
+          // on LDS dominated the FMA phase)
+          float4 bb[4], av[RT];
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) bb[kk] = *reinterpret_cast<const float4 *>(Bm + kk * mp + c0);
+#pragma unroll
+          for (int x = 0; x < RT; ++x) av[x] = *reinterpret_cast<const float4 *>(src + x * RS * ld);
+#pragma unroll 2
           for (int k = 0; k < K; k += 4) {
-            float4 bb[4];
+            float4 nb[4], na[RT];
+            const int kn = k + 4 < K ? k + 4 : k;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              bb[kk] = *reinterpret_cast<const float4 *>(Bm + (k + kk) * mp + c0);
+              nb[kk] = *reinterpret_cast<const float4 *>(Bm + (kn + kk) * mp + c0);
+#pragma unroll
+            for (int x = 0; x < RT; ++x)
+              na[x] = *reinterpret_cast<const float4 *>(src + x * RS * ld + kn);
 #pragma unroll
             for (int x = 0; x < RT; ++x) {
-              const float4 av = *reinterpret_cast<const float4 *>(src + x * RS * ld + k);
-              const float aa[4] = {av.x, av.y, av.z, av.w};
+              const float aa[4] = {av[x].x, av[x].y, av[x].z, av[x].w};
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
                 acc[x][0] += aa[kk] * bb[kk].x;
@@ -643,6 +654,10 @@ __global__ void __launch_bounds__(kWsF + kWsS, 1)
                 acc[x][3] += aa[kk] * bb[kk].w;
               }
             }
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) bb[kk] = nb[kk];
+#pragma unroll
+            for (int x = 0; x < RT; ++x) av[x] = na[x];
           }
           float *dst = (phase == 0 ? oP(o, mat) : oX(o, mat)) + rb * mp + c0;
 #pragma unroll
