@@ -221,6 +221,11 @@ int mg_embed_host(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *
 int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float *S,
                      const float *AS, const float *b, double *GB, double *GA);
 
+/* Host <-> device copies for large pageable host buffers (results, inputs):
+ * pipelined through the context's pinned stages; blocking. */
+int mg_copy_d2h(mg_ctx *ctx, void *host, const void *dev, int64_t bytes);
+int mg_copy_h2d(mg_ctx *ctx, void *dev, const void *host, int64_t bytes);
+
 /* numpy's Generator(PCG64).standard_normal stream, bit for bit, on the device:
  * the reference's initial block (eigensolver.py:177-178, 189) is the first
  * n*m values of default_rng(seed).standard_normal.  (state, inc) are the 128-bit
