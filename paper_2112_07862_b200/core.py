@@ -114,13 +114,22 @@ def _normals(seed: int, count: int):
     if os.environ.get("MG_HOST_NORMALS", "0") == "1":
         z = np.random.default_rng(seed).standard_normal(count)
         return _dev(z, _t().float64), count
+    return _normals_on(0, seed, count), count
+
+
+def _normals_on(device: int, seed: int, count: int, ctx=None):
+    """The same stream generated on CUDA device ``device`` through library context
+    ``ctx`` (default: the process-wide context of that device)."""
+    torch = _t()
     st = np.random.default_rng(seed).bit_generator.state["state"]
     m64 = (1 << 64) - 1
     s, inc = int(st["state"]), int(st["inc"])
-    out = _empty(count, _t().float64)
-    _call("mg_normal_stream", _ctx(), C.c_uint64(s >> 64), C.c_uint64(s & m64),
-          C.c_uint64(inc >> 64), C.c_uint64(inc & m64), count, _ptr(out))
-    return out[:count] if count else out, count
+    out = torch.empty(max(int(count), 1), dtype=torch.float64, device=torch.device("cuda", device))
+    torch.cuda.synchronize(device)
+    _call("mg_normal_stream", ctx if ctx is not None else N.context(device),
+          C.c_uint64(s >> 64), C.c_uint64(s & m64),
+          C.c_uint64(inc >> 64), C.c_uint64(inc & m64), int(count), _ptr(out))
+    return out[:count] if count else out
 
 
 # ------------------------------------------------------------------- types ---

@@ -132,7 +132,7 @@ def embed_arrays_dist(comm: Comm, ctx, device: int, n, indptr, indices, weights,
         i = torch.from_numpy(np.ascontiguousarray(indices, dtype=np.int64)).to(dev)
         w = torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float64)).to(dev)
         nz = _core._stream_size(n, max(m, min(8, max(n - 1, 1))))
-        z = torch.from_numpy(np.random.default_rng(cfg.seed).standard_normal(nz)).to(dev)
+        z = _core._normals_on(device, cfg.seed, nz, ctx)  # numpy's stream, on this GPU / context
     else:
         p, i, w, z = device_inputs
         nz = int(z.numel())
