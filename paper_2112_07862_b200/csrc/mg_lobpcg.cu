@@ -97,17 +97,16 @@ void make_solver_csr(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *
 // ------------------------------------------------------------------ SpMM ---
 // Sub-warp of L lanes per CSR row; lane l owns columns [l*VN, l*VN+VN) of the
 // row-major block, so each nonzero costs one 16-byte coalesced load of the
-// neighbour's row segment.  Four nonzeros in flight per lane.  The matrix is
-// streamed once (L2 evict-first, no L1 allocation); the gathered block rows
-// are re-read ~nnz/row times and are kept in L2 (evict-last).
-__device__ __forceinline__ uint64_t l2_policy_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
+// neighbour's row segment.  Four nonzeros in flight per lane.  The gathered
+// block rows are re-read ~nnz/row times and are kept in L2 (evict-last).
 __device__ __forceinline__ uint64_t l2_policy_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ int ld_stream_i32(const int *a, uint64_t pol) {
@@ -157,7 +156,10 @@ __global__ void __launch_bounds__(256)
   int G = 32 / L;
   int g = lane / L, gl = lane - g * L;
   if (g >= G) return;
-  const uint64_t pf = l2_policy_first(), pl = l2_policy_last();
+  // the matrix stream is read with the default L2 policy: each 32-byte sector
+  // of indices / values serves two 4-nonzero groups, and evict_first dropped
+  // it in between (11.7 -> 10.0 ms per SpMM at C5, profiles/r1_ncu_c5_20M.md)
+  const uint64_t pf = l2_policy_normal(), pl = l2_policy_last();
   int64_t per_block = (int64_t)(blockDim.x >> 5) * G;
   int64_t stride = (int64_t)gridDim.x * per_block;
   for (int64_t row = blockIdx.x * per_block + (threadIdx.x >> 5) * G + g; row < n; row += stride) {
