@@ -475,7 +475,11 @@ __global__ void k_reduce_gram_tc(const double *__restrict__ part, int npairs, in
 //   loads, 32 K per stage); B operand: [Zp | Zx] pieces resident in smem.
 static constexpr int kUpM = 128;      // rows per tile (MMA M)
 static constexpr int kUpN = 80;       // [P | X] columns (2 * mp <= 80), zero-padded
-static constexpr int kUpKC = 32;      // K per stage
+// K per stage: 32 with 2 pieces, 16 with 3 (operand shared memory)
+template <int NP>
+struct UpCfg {
+  static constexpr int KC = NP == 3 ? 16 : 32;
+};
 static constexpr int kUpKmax = 112;   // w <= 112
 static constexpr int kUpThreads = 256;
 
@@ -488,9 +492,11 @@ struct UpdTcArgs {
 };
 
 __host__ __device__ constexpr size_t up_b_piece() { return (size_t)kUpN * kUpKmax * 4; }
-__host__ __device__ constexpr size_t up_a_piece() { return (size_t)kUpM * kUpKC * 4; }
+template <int NP>
+__host__ __device__ constexpr size_t up_a_piece() { return (size_t)kUpM * UpCfg<NP>::KC * 4; }
+template <int NP>
 __host__ __device__ constexpr size_t up_smem() {
-  return 2 * up_b_piece() + 2 * 4 * up_a_piece() + 64 * 4 + 16 * 8 + 16;
+  return NP * up_b_piece() + 2 * 2 * NP * up_a_piece<NP>() + 64 * 4 + 16 * 8 + 16;
 }
 
 __device__ __forceinline__ void tmem_ld2(uint32_t taddr, float *v) {
@@ -503,15 +509,18 @@ __device__ __forceinline__ void tmem_ld2(uint32_t taddr, float *v) {
   v[1] = __uint_as_float(r1);
 }
 
+template <int NP>
 __global__ void __launch_bounds__(kUpThreads, 1)
     k_update_tc(float *__restrict__ S, float *__restrict__ AS, const float *__restrict__ b,
                 const float *__restrict__ prec, const float *__restrict__ Mg,
                 const double *__restrict__ theta, UpdTcArgs a) {
   if (*a.skip) return;
   extern __shared__ __align__(1024) unsigned char sm[];
-  unsigned char *zb = sm;                          // [Zp|Zx] hi, lo (K-major, N=80 x K=112)
-  unsigned char *st0 = sm + 2 * up_b_piece();      // 2 stages x [S hi, S lo, AS hi, AS lo]
-  float *sth = reinterpret_cast<float *>(st0 + 2 * 4 * up_a_piece());  // theta (mp <= 40)
+  constexpr int kUpKC = UpCfg<NP>::KC;
+  constexpr size_t APC = up_a_piece<NP>();
+  unsigned char *zb = sm;                           // [Zp|Zx] NP pieces (K-major, N=80 x K=112)
+  unsigned char *st0 = sm + NP * up_b_piece();      // 2 stages x [S pieces, AS pieces]
+  float *sth = reinterpret_cast<float *>(st0 + 2 * 2 * NP * APC);  // theta (mp <= 40)
   uint64_t *bars = reinterpret_cast<uint64_t *>(sth + 64);
   uint64_t *st_empty = bars, *tm_full = bars + 2, *tm_empty = bars + 4;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 8);
@@ -532,10 +541,10 @@ __global__ void __launch_bounds__(kUpThreads, 1)
       }
     }
     float p[3];
-    split_tf32<2>(v, p);
+    split_tf32<NP>(v, p);
     const int off = ((n >> 3) * 128 + (n & 7) * 16 + (k >> 2) * LBO_B + (k & 3) * 4) >> 2;
-    reinterpret_cast<float *>(zb)[off] = p[0];
-    reinterpret_cast<float *>(zb + up_b_piece())[off] = p[1];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) reinterpret_cast<float *>(zb + q * up_b_piece())[off] = p[q];
   }
   for (int e = tid; e < 64; e += kUpThreads) sth[e] = e < m ? (float)theta[e] : 0.f;
   if (tid == 0) {
@@ -569,13 +578,14 @@ __global__ void __launch_bounds__(kUpThreads, 1)
 #pragma unroll
   for (int j = 0; j < 18; ++j) sr[j] = sx[j] = 0.f;
 
-  float4 ld_s[4], ld_a[4];  // this thread's share of one K stage (S and AS)
-  // item j (0..3): row = warp * 16 + (j >> 1) * 8 + lane % 8 ... covering 128 rows
+  // one K stage = 128 rows x kUpKC columns of S and AS: CPR 16-byte chunks
+  // per row, J per thread; item e = tid + 256 j -> (row e / CPR, chunk e % CPR)
+  constexpr int CPR = kUpKC / 4, J = kUpM * CPR / kUpThreads;
+  float4 ld_s[J], ld_a[J];
   auto load_stage = [&](int64_t row0, int kc) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = warp * 16 + (j >> 1) * 8 + (lane & 7);
-      const int c4 = (lane >> 3) + 4 * (j & 1);  // 0..7
+    for (int j = 0; j < J; ++j) {
+      const int e = tid + kUpThreads * j, r = e / CPR, c4 = e % CPR;
       const int col = kc * kUpKC + c4 * 4;
       const int64_t row = row0 + r;
       float4 vs = make_float4(0.f, 0.f, 0.f, 0.f), va = vs;
@@ -588,28 +598,27 @@ __global__ void __launch_bounds__(kUpThreads, 1)
     }
   };
   auto store_stage = [&](int st) {
-    unsigned char *base = st0 + (size_t)st * 4 * up_a_piece();
+    unsigned char *base = st0 + (size_t)st * 2 * NP * APC;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = warp * 16 + (j >> 1) * 8 + (lane & 7);
-      const int c4 = (lane >> 3) + 4 * (j & 1);
+    for (int j = 0; j < J; ++j) {
+      const int e = tid + kUpThreads * j, r = e / CPR, c4 = e % CPR;
       const int off = (r >> 3) * 128 + (r & 7) * 16 + c4 * LBO_A;
       float ps[4][3], pa[4][3];
-      split_tf32<2>(ld_s[j].x, ps[0]);
-      split_tf32<2>(ld_s[j].y, ps[1]);
-      split_tf32<2>(ld_s[j].z, ps[2]);
-      split_tf32<2>(ld_s[j].w, ps[3]);
-      split_tf32<2>(ld_a[j].x, pa[0]);
-      split_tf32<2>(ld_a[j].y, pa[1]);
-      split_tf32<2>(ld_a[j].z, pa[2]);
-      split_tf32<2>(ld_a[j].w, pa[3]);
-      *reinterpret_cast<float4 *>(base + off) = make_float4(ps[0][0], ps[1][0], ps[2][0], ps[3][0]);
-      *reinterpret_cast<float4 *>(base + up_a_piece() + off) =
-          make_float4(ps[0][1], ps[1][1], ps[2][1], ps[3][1]);
-      *reinterpret_cast<float4 *>(base + 2 * up_a_piece() + off) =
-          make_float4(pa[0][0], pa[1][0], pa[2][0], pa[3][0]);
-      *reinterpret_cast<float4 *>(base + 3 * up_a_piece() + off) =
-          make_float4(pa[0][1], pa[1][1], pa[2][1], pa[3][1]);
+      split_tf32<NP>(ld_s[j].x, ps[0]);
+      split_tf32<NP>(ld_s[j].y, ps[1]);
+      split_tf32<NP>(ld_s[j].z, ps[2]);
+      split_tf32<NP>(ld_s[j].w, ps[3]);
+      split_tf32<NP>(ld_a[j].x, pa[0]);
+      split_tf32<NP>(ld_a[j].y, pa[1]);
+      split_tf32<NP>(ld_a[j].z, pa[2]);
+      split_tf32<NP>(ld_a[j].w, pa[3]);
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        *reinterpret_cast<float4 *>(base + q * APC + off) =
+            make_float4(ps[0][q], ps[1][q], ps[2][q], ps[3][q]);
+        *reinterpret_cast<float4 *>(base + (NP + q) * APC + off) =
+            make_float4(pa[0][q], pa[1][q], pa[2][q], pa[3][q]);
+      }
     }
   };
   // epilogue of tile tt (TMEM buffer buf): thread = (row q*32+lane, 18 columns)
@@ -697,24 +706,41 @@ __global__ void __launch_bounds__(kUpThreads, 1)
         if (kc == 0) mbar_wait(&tm_empty[buf], ((ti >> 1) & 1) ^ 1);
         tc_fence_after();
         const int ksteps = min(kUpKC, w - kc * kUpKC + 7) / 8;  // 8-row K steps in this stage
-        const uint32_t A = st_base + st * 4 * (uint32_t)up_a_piece();
+        const uint32_t A = st_base + st * 2 * NP * (uint32_t)APC;
         const uint32_t dS = tbase + buf * 256, dA = dS + 80, dA2 = dS + 160;
         for (int s = 0; s < ksteps; ++s) {
           const uint32_t kb = (uint32_t)(kc * (kUpKC / 4) + 2 * s) * LBO_B;  // B: K offset
-          const uint64_t bh = dB0 | ((zb_base + kb) >> 4);
-          const uint64_t bl = dB0 | ((zb_base + (uint32_t)up_b_piece() + kb) >> 4);
           const uint32_t ka = 2 * s * LBO_A;
-          const uint64_t sh = dA0 | ((A + ka) >> 4);
-          const uint64_t sl = dA0 | ((A + (uint32_t)up_a_piece() + ka) >> 4);
-          const uint64_t ah = dA0 | ((A + 2 * (uint32_t)up_a_piece() + ka) >> 4);
-          const uint64_t al = dA0 | ((A + 3 * (uint32_t)up_a_piece() + ka) >> 4);
+          uint64_t bq[NP], sq[NP], aq[NP];
+#pragma unroll
+          for (int q = 0; q < NP; ++q) {
+            bq[q] = dB0 | ((zb_base + q * (uint32_t)up_b_piece() + kb) >> 4);
+            sq[q] = dA0 | ((A + q * (uint32_t)APC + ka) >> 4);
+            aq[q] = dA0 | ((A + (NP + q) * (uint32_t)APC + ka) >> 4);
+          }
           const uint32_t acc = (kc == 0 && s == 0) ? 0u : 1u;
-          umma_tf32(dS, sl, bh, idesc, acc);  // small products first
-          umma_tf32(dS, sh, bl, idesc, 1u);
-          umma_tf32(dS, sh, bh, idesc, 1u);
-          umma_tf32(dA2, al, bh, idesc, acc);
-          umma_tf32(dA2, ah, bl, idesc, 1u);
-          umma_tf32(dA, ah, bh, idesc, acc);
+          // small products first; NP = 3 keeps every (i, j) with i + j < 3 plus (1, 1)
+          if (NP == 3) {
+            umma_tf32(dS, sq[2], bq[0], idesc, acc);
+            umma_tf32(dS, sq[0], bq[2], idesc, 1u);
+            umma_tf32(dS, sq[1], bq[1], idesc, 1u);
+            umma_tf32(dS, sq[1], bq[0], idesc, 1u);
+            umma_tf32(dS, sq[0], bq[1], idesc, 1u);
+            umma_tf32(dS, sq[0], bq[0], idesc, 1u);
+            umma_tf32(dA2, aq[2], bq[0], idesc, acc);
+            umma_tf32(dA2, aq[0], bq[2], idesc, 1u);
+            umma_tf32(dA2, aq[1], bq[1], idesc, 1u);
+            umma_tf32(dA2, aq[1], bq[0], idesc, 1u);
+            umma_tf32(dA2, aq[0], bq[1], idesc, 1u);
+            umma_tf32(dA, aq[0], bq[0], idesc, acc);
+          } else {
+            umma_tf32(dS, sq[1], bq[0], idesc, acc);
+            umma_tf32(dS, sq[0], bq[1], idesc, 1u);
+            umma_tf32(dS, sq[0], bq[0], idesc, 1u);
+            umma_tf32(dA2, aq[1], bq[0], idesc, acc);
+            umma_tf32(dA2, aq[0], bq[1], idesc, 1u);
+            umma_tf32(dA, aq[0], bq[0], idesc, acc);
+          }
         }
         umma_commit(&st_empty[st]);
         if (kc == nkc - 1) umma_commit(&tm_full[buf]);
@@ -775,13 +801,22 @@ int update_tc(mg_ctx *ctx, int64_t n, int ld, int w, int m, int mp, float *S, fl
   a.wc = wc;
   const int64_t ntiles = (n + kUpM - 1) / kUpM;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ctx->num_sms));
+  static const int np = [] {
+    const char *e = getenv("MG_TC_UPD_PIECES");
+    return (e && e[0] == '2') ? 2 : 3;
+  }();
   static thread_local bool attr = false;
   if (!attr) {
-    MG_CUDA(cudaFuncSetAttribute(k_update_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)up_smem()));
+    MG_CUDA(cudaFuncSetAttribute(k_update_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)up_smem<2>()));
+    MG_CUDA(cudaFuncSetAttribute(k_update_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)up_smem<3>()));
     attr = true;
   }
-  k_update_tc<<<grid, kUpThreads, up_smem(), ctx->stream>>>(S, AS, b, prec, M, theta, a);
+  if (np == 3)
+    k_update_tc<3><<<grid, kUpThreads, up_smem<3>(), ctx->stream>>>(S, AS, b, prec, M, theta, a);
+  else
+    k_update_tc<2><<<grid, kUpThreads, up_smem<2>(), ctx->stream>>>(S, AS, b, prec, M, theta, a);
   MG_CHECK_LAUNCH(ctx);
   return grid;
 }
