@@ -390,14 +390,23 @@ __global__ void k_yaxpy(int64_t n, T *__restrict__ S, int ld, int ycol, int c_lo
   }
 }
 
+// column sums of per-block partials [nb][w]: one warp per column, lanes take
+// strided blocks in a fixed order and a fixed xor tree combines them, so the
+// result is run-to-run deterministic (one thread per column serialised ~600
+// dependent loads: ~50 us per call)
 __global__ void k_reduce_cols(const double *__restrict__ part, int nb, int w,
                               double *__restrict__ out) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < w; t += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < w;
+       t += (gridDim.x * blockDim.x) >> 5) {
     double s = 0.0;
-    for (int q = 0; q < nb; ++q) s += part[(int64_t)q * w + t];
-    out[t] = s;
+    for (int q = lane; q < nb; q += 32) s += part[(int64_t)q * w + t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[t] = s;
   }
 }
+static inline int reduce_cols_grid(int w) { return (w + 7) / 8; }
 
 // X0 from the normal stream: S[r][c0 + c] = z[off + r*w + c]  (row-major (n, w))
 template <typename T>
@@ -1065,7 +1074,7 @@ struct Lobpcg {
                                             sp.jacobi ? prec.p : nullptr, write_w ? S.p : nullptr,
                                             colpart.p, Wc.p);
     MG_CHECK_LAUNCH(ctx);
-    k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, nb, 2 * mp, colred.p);
+    k_reduce_cols<<<reduce_cols_grid(2 * mp), 256, 0, ctx->stream>>>(colpart.p, nb, 2 * mp, colred.p);
     MG_CHECK_LAUNCH(ctx);
     ar(colred.p, 2 * mp);
     out.resize(2 * mp);
@@ -1080,7 +1089,7 @@ struct Lobpcg {
     k_coldot<T><<<nb, R * mp, (size_t)R * mp * sizeof(double), ctx->stream>>>(n, S.p, AS.p, ld,
                                                                               mp, colpart.p);
     MG_CHECK_LAUNCH(ctx);
-    k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, nb, mp, theta.p);
+    k_reduce_cols<<<reduce_cols_grid(mp), 256, 0, ctx->stream>>>(colpart.p, nb, mp, theta.p);
     MG_CHECK_LAUNCH(ctx);
     ar(theta.p, mp);
     th.resize(mp);
@@ -1117,7 +1126,7 @@ struct Lobpcg {
     if (ypart.n < (size_t)nb * region_w) ypart.alloc(ctx, (size_t)nb * region_w);
     k_ydot<T><<<nb, 256, 0, ctx->stream>>>(n, S.p, ld, bw.p, 3 * mp, region0, region_w, ypart.p);
     MG_CHECK_LAUNCH(ctx);
-    k_reduce_cols<<<1, 256, 0, ctx->stream>>>(ypart.p, nb, region_w, Gr0.p);
+    k_reduce_cols<<<reduce_cols_grid(region_w), 256, 0, ctx->stream>>>(ypart.p, nb, region_w, Gr0.p);
     MG_CHECK_LAUNCH(ctx);
     ar(Gr0.p, (size_t)region_w);
     k_yaxpy<T><<<grid_for(n * (c_hi - c_lo), 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
@@ -1247,7 +1256,7 @@ struct Lobpcg {
                                             sp.jacobi ? prec.p : nullptr, write_w ? S.p : nullptr,
                                             colpart.p, Wc.p);
     MG_CHECK_LAUNCH(ctx);
-    k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, nb, 2 * mp, colred.p);
+    k_reduce_cols<<<reduce_cols_grid(2 * mp), 256, 0, ctx->stream>>>(colpart.p, nb, 2 * mp, colred.p);
     MG_CHECK_LAUNCH(ctx);
     ar(colred.p, 2 * mp);
     MG_CUDA(cudaMemcpyAsync(colred.p + 2 * mp, theta.p, mp * sizeof(double),
@@ -1529,7 +1538,7 @@ struct Lobpcg {
       for (int q = 21; q < 26; ++q) fprintf(stderr, " %.1f", (clk[q] - clk[q - 1]) / 1e3);
       fprintf(stderr, "\n");
     }
-    k_reduce_cols<<<1, 256, 0, ctx->stream>>>(colpart.p, nblk_upd, 2 * mp, colred.p);
+    k_reduce_cols<<<reduce_cols_grid(2 * mp), 256, 0, ctx->stream>>>(colpart.p, nblk_upd, 2 * mp, colred.p);
     MG_CHECK_LAUNCH(ctx);
     ar(colred.p, 2 * mp);
     MG_CUDA(cudaMemcpyAsync(colred.p + 2 * mp, theta.p, mp * sizeof(double),
