@@ -111,10 +111,12 @@ __device__ inline void blk_eig_smallest(double *A, int lda, int n, int nev, doub
     const double K = 0.5 * tk * blk_sum(s2, wp);
     for (int i = tid; i < m; i += nt) p[i] -= K * x[i * lda];
     __syncthreads();
+    // rank-2 update, one warp per row (no per-element integer division)
     double *A22w = A + (k + 1) * lda + (k + 1);
-    for (int e2 = tid; e2 < m * m; e2 += nt) {
-      const int r = e2 / m, c = e2 - r * m;
-      A22w[r * lda + c] -= x[r * lda] * p[c] + p[r] * x[c * lda];
+    for (int r = warp; r < m; r += nw) {
+      const double xr = x[r * lda], pr = p[r];
+      double *row = A22w + r * lda;
+      for (int c = lane; c < m; c += 32) row[c] -= xr * p[c] + pr * x[c * lda];
     }
     __syncthreads();
   }
@@ -274,9 +276,10 @@ __device__ inline void blk_eig_smallest(double *A, int lda, int n, int nev, doub
       if (lane == 0) p[j] = tk * s;
     }
     __syncthreads();
-    for (int e2 = tid; e2 < m * nev; e2 += nt) {
-      const int i = e2 / nev, j = e2 - i * nev;
-      Z[(k + 1 + i) * ldz + j] -= v[i * lda] * p[j];
+    for (int i = warp; i < m; i += nw) {
+      const double vi = v[i * lda];
+      double *zr = Z + (k + 1 + i) * ldz;
+      for (int j = lane; j < nev; j += 32) zr[j] -= vi * p[j];
     }
     __syncthreads();
   }
