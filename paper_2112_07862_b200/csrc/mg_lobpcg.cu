@@ -1342,7 +1342,11 @@ struct Lobpcg {
     // output tiles fit with >= 32-row tiles
     upd_ws = false;
     if (sizeof(T) == 4 && env_double("MG_UPD_WS", 1) != 0 && mp % 4 == 0) {
-      for (int tk = 64; tk >= 32; tk -= 4)
+      // MG_UPD_WS_TKMAX=256 lets narrow blocks (K = 8) use it with taller tiles:
+      // the update kernel itself is 25 % faster at C3 but the embed measured
+      // slower (1.25 -> 1.60 s), so the default keeps them on k_update_resid
+      const int tk_max = (int)env_double("MG_UPD_WS_TKMAX", 64);
+      for (int tk = tk_max; tk >= 32; tk -= 4)
         if (upd_ws_bytes(tk, ld, 3 * mp, mp) <= budget && (tk / 4) * ((mp + 3) / 4) * 2 >= 128) {
           upd_ws = true;
           tk_ws = tk;
