@@ -1342,10 +1342,11 @@ struct Lobpcg {
     // output tiles fit with >= 32-row tiles
     upd_ws = false;
     if (sizeof(T) == 4 && env_double("MG_UPD_WS", 1) != 0 && mp % 4 == 0) {
-      // MG_UPD_WS_TKMAX=256 lets narrow blocks (K = 8) use it with taller tiles:
-      // the update kernel itself is 25 % faster at C3 but the embed measured
-      // slower (1.25 -> 1.60 s), so the default keeps them on k_update_resid
-      const int tk_max = (int)env_double("MG_UPD_WS_TKMAX", 64);
+      // narrow blocks (K = 8, the eps solve's block) need taller tiles to give
+      // the FMA warps >= 128 jobs: 25 % faster updates and ~10 % off C3's solve
+      // (the outputs are the same fma chains as k_update_resid's); wide blocks
+      // are capped by shared memory (52 rows at m = 33)
+      const int tk_max = (int)env_double("MG_UPD_WS_TKMAX", 256);
       for (int tk = tk_max; tk >= 32; tk -= 4)
         if (upd_ws_bytes(tk, ld, 3 * mp, mp) <= budget && (tk / 4) * ((mp + 3) / 4) * 2 >= 128) {
           upd_ws = true;
