@@ -521,6 +521,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
 // Barriers: full[s] (TMA), rdy[o] (8 FMA warps -> output tile o complete),
 // fre[o] (4 store warps -> output tile o consumed, stage refilled).
 constexpr int kWsF = 256, kWsS = 128;
+#ifndef MG_WS_NS
+#define MG_WS_NS 2
+#endif
+constexpr int kWsNS = MG_WS_NS;  // TMA ring stages (one tile of look-ahead covers the latency)
 
 __device__ __forceinline__ void mbar_arrive_cta(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -528,7 +532,7 @@ __device__ __forceinline__ void mbar_arrive_cta(uint64_t *bar) {
 
 __host__ __device__ inline size_t upd_ws_bytes(int tk, int ld, int w, int mp) {
   const size_t tile = (size_t)tk * ld + 16;
-  return (size_t)3 * (2 * tile + tk + 16) * 4 + ((size_t)w * mp + (size_t)mp * mp + 16) * 4 +
+  return (size_t)kWsNS * (2 * tile + tk + 16) * 4 + ((size_t)w * mp + (size_t)mp * mp + 16) * 4 +
          (size_t)8 * tk * mp * 4 + (size_t)(mp + 4) * 4 + 256;
 }
 
@@ -538,7 +542,7 @@ __global__ void __launch_bounds__(kWsF + kWsS, 1)
                 const float *__restrict__ prec, const float *__restrict__ Mg,
                 const double *__restrict__ theta, UpdArgs a) {
   if (*a.skip) return;
-  constexpr int NS = 3;
+  constexpr int NS = kWsNS;
   extern __shared__ __align__(128) unsigned char smraw[];
   const int ld = a.ld, w = a.w, mp = a.mp, TK = a.tk;
   const size_t tile_elems = (size_t)TK * ld + 16;

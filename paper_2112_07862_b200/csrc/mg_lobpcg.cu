@@ -1346,14 +1346,29 @@ struct Lobpcg {
       // the FMA warps >= 128 jobs: 25 % faster updates and ~10 % off C3's solve
       // (the outputs are the same fma chains as k_update_resid's); wide blocks
       // are capped by shared memory (52 rows at m = 33)
+      // Among the tile heights that fit, take the one that best fills the 256 FMA
+      // threads (jobs / whole rounds); ties go to the taller tile.  At m = 33 that
+      // is 56 rows (252 jobs) with the two-stage ring.
       const int tk_max = (int)env_double("MG_UPD_WS_TKMAX", 256);
-      for (int tk = tk_max; tk >= 32; tk -= 4)
-        if (upd_ws_bytes(tk, ld, 3 * mp, mp) <= budget && (tk / 4) * ((mp + 3) / 4) * 2 >= 128) {
+      double best = 0.0;
+      for (int tk = tk_max; tk >= 32; tk -= 4) {
+        const int jobs = (tk / 4) * ((mp + 3) / 4) * 2;
+        if (upd_ws_bytes(tk, ld, 3 * mp, mp) > budget || jobs < 128) continue;
+        const double fill = (double)jobs / (double)(((jobs + kWsF - 1) / kWsF) * kWsF);
+        if (fill > best + 1e-9) {
+          best = fill;
           upd_ws = true;
           tk_ws = tk;
           ws_smem = upd_ws_bytes(tk, ld, 3 * mp, mp);
-          break;
         }
+      }
+      if (const char *e = getenv("MG_UPD_WS_TK")) {
+        const int tk = atoi(e);
+        if (tk >= 4 && upd_ws_bytes(tk, ld, 3 * mp, mp) <= budget) {
+          tk_ws = tk;
+          ws_smem = upd_ws_bytes(tk, ld, 3 * mp, mp);
+        }
+      }
       if (upd_ws)
         MG_CUDA(cudaFuncSetAttribute(k_update_ws<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)ws_smem));
