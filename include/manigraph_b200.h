@@ -140,9 +140,12 @@ typedef struct mg_solver_cfg {
 } mg_solver_cfg;
 
 typedef struct mg_solver_out {
-  double *eigenvalues;      /* host k */
-  double *residual_norms;   /* host k */
-  int32_t *converged;       /* host k */
+  /* mg_lobpcg: k entries each.  mg_embed / mg_embed_host: eigenvalues K
+   * (K+1 with cfg->reserved == 1); residual_norms and converged always K+1
+   * (the solver's view, including the dropped pair). */
+  double *eigenvalues;      /* host */
+  double *residual_norms;   /* host */
+  int32_t *converged;       /* host */
   double *history;          /* host, capacity history_cap (ritz_sum_history) */
   int32_t history_cap;
   int32_t iterations;       /* out */
@@ -161,6 +164,17 @@ int mg_lobpcg(mg_ctx *ctx, int64_t n, const int64_t *a_indptr, const int64_t *a_
               const double *a_data, const double *b, const mg_solver_cfg *cfg,
               const double *normals, int64_t n_normals, const double *deflate,
               double *eigenvectors, mg_solver_out *out);
+
+/* lobpcg_smallest with several deflation vectors (eigensolver.py:179-184,
+ * 189-192, 239-241: `for col in defl.T: block = _b_project_out(col, block)`).
+ * `deflate` is device n x n_deflate COLUMN-major (vector j at deflate + j*n);
+ * the vectors are projected out one after another in that order, exactly as
+ * the reference does (no joint orthogonalisation).  mg_lobpcg is the
+ * n_deflate <= 1 case. */
+int mg_lobpcg_deflate(mg_ctx *ctx, int64_t n, const int64_t *a_indptr, const int64_t *a_indices,
+                      const double *a_data, const double *b, const mg_solver_cfg *cfg,
+                      const double *normals, int64_t n_normals, const double *deflate,
+                      int32_t n_deflate, double *eigenvectors, mg_solver_out *out);
 
 /* smallest_above_null (eigensolver.py:431-460) as used by identity_shift
  * (operators.py:138-156): smallest eigenvalue of Q above tau = 1e-8 tr(Q)/n,
@@ -192,9 +206,13 @@ typedef struct mg_embed_diag {
 } mg_embed_diag;
 
 /* embed (embedding.py:77-103): components check, build_operator_pair,
- * K+1-pair LOBPCG, drop the first pair.  P: device n x K row-major;
- * eigenvalues host K; b device n.  `normals` as in mg_lobpcg (needs
- * n * max(K+1, 8) entries).  check_connected = 0 bypasses the component test
+ * K+1-pair LOBPCG, drop the first pair.  P: device n x K row-major (n x (K+1)
+ * with cfg->reserved == 1); eigenvalues host K (K+1); b device n.  `normals`
+ * as in mg_lobpcg: the eps solve may double its block from 8 to 64 and
+ * refills continue the stream, so pass at least n * max(K+1, 64) entries
+ * plus a refill margin; a short stream fails with MG_ERR_INPUT ("normal
+ * stream exhausted") and the caller retries with a longer one (core.embed
+ * does).  check_connected = 0 bypasses the component test
  * (SURVEY F6, config 4).  Returns MG_ERR_NOT_CONVERGED (outputs filled) when
  * require_convergence and some pair is unconverged. */
 int mg_embed(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,

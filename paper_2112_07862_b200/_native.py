@@ -74,6 +74,8 @@ SIGNATURES = {
     "mg_disc_left_min": [vp, i64, vp, vp, vp, P_f64, P_i64],
     "mg_lobpcg": [vp, i64, vp, vp, vp, vp, C.POINTER(SolverCfg), vp, i64, vp, vp,
                   C.POINTER(SolverOut)],
+    "mg_lobpcg_deflate": [vp, i64, vp, vp, vp, vp, C.POINTER(SolverCfg), vp, i64, vp, i32, vp,
+                          C.POINTER(SolverOut)],
     "mg_identity_shift": [vp, i64, vp, vp, vp, vp, i64, i32, P_f64],
     "mg_smallest_above_null": [vp, i64, vp, vp, vp, f64, f64, i32, vp, i64, i32, P_f64],
     "mg_spmm": [vp, i64, vp, vp, vp, vp, i32, vp],

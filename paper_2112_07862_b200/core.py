@@ -589,12 +589,15 @@ def lobpcg_smallest(a, b, cfg: SolverConfig, deflate=None) -> EigenResult:
     bvec = _bvec(b, n)
     if cfg.k > n:
         raise InputError(f"block size {cfg.k} exceeds dimension {n}")
-    dvec = None
+    dvec, ndefl = None, 0
     if deflate is not None:
+        # eigensolver.py:179-184: columns projected out one after another
         defl = np.atleast_2d(np.asarray(deflate, dtype=np.float64).T).T
-        if defl.shape[1] != 1:
-            raise InputError("only a single deflation vector is supported")
-        dvec = _dev(defl[:, 0], torch.float64)
+        if defl.shape[0] != n:
+            raise InputError(f"deflation vectors have {defl.shape[0]} rows, expected {n}")
+        ndefl = int(defl.shape[1])
+        if ndefl:
+            dvec = _dev(np.ascontiguousarray(defl.T).ravel(), torch.float64)  # column-major
     p, i, d = a._device()
     bd = _dev(bvec, torch.float64)
     k = int(cfg.k)
@@ -615,14 +618,16 @@ def lobpcg_smallest(a, b, cfg: SolverConfig, deflate=None) -> EigenResult:
         z, nz = _normals(cfg.seed, count)
         _sync()
         try:
-            N.call("mg_lobpcg", _ctx(), n, _ptr(p), _ptr(i), _ptr(d), _ptr(bd), C.byref(s), _ptr(z),
-                   nz, _ptr(dvec), _ptr(vecs), C.byref(out))
+            N.call("mg_lobpcg_deflate", _ctx(), n, _ptr(p), _ptr(i), _ptr(d), _ptr(bd), C.byref(s),
+                   _ptr(z), nz, _ptr(dvec), ndefl, _ptr(vecs), C.byref(out))
             break
         except N.NativeError as e:
             if "stream exhausted" in str(e):
                 count *= 8
                 continue
             _raise_native(e)
+    else:
+        raise InputError("normal stream exhausted")
     return EigenResult(eigenvalues=ev.copy(), eigenvectors=_host(vecs[:n * k].view(n, k)),
                        iterations=int(out.iterations), residual_norms=rn.copy(),
                        converged=cv.astype(bool), ritz_sum_history=list(hist[:out.history_len]))

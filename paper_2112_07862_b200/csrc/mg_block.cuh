@@ -79,7 +79,9 @@ struct SolveSpec {
   bool jacobi = true;
   const double *normals = nullptr;  // device, standard-normal stream
   int64_t n_normals = 0;
-  const double *deflate = nullptr;  // device n (one vector) or null
+  const double *deflate = nullptr;  // device: n_deflate vectors (vector j at deflate + j * deflate_ld) or null
+  int n_deflate = 1;
+  int64_t deflate_ld = 0;
   const int64_t *perm = nullptr;    // optional: solver row r is original row perm[r]
   // distributed mode (mg_dist.cuh): communicator and this rank's DistPart<T>;
   // rows are the global rows [row_base, row_base + n_local)

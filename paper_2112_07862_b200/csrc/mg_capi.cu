@@ -102,7 +102,8 @@ struct SolverIn {
 static SolveResult run_lobpcg(mg_ctx *ctx, const SolverIn &a, const double *b,
                               const mg_solver_cfg &cfg, const double *normals, int64_t n_normals,
                               const double *deflate, double *eigvecs,
-                              const int64_t *perm = nullptr, Comm *comm = nullptr) {
+                              const int64_t *perm = nullptr, Comm *comm = nullptr,
+                              int n_deflate = 1) {
   SolveSpec sp;
   sp.perm = perm;
   sp.k = cfg.k;
@@ -112,6 +113,8 @@ static SolveResult run_lobpcg(mg_ctx *ctx, const SolverIn &a, const double *b,
   sp.normals = normals;
   sp.n_normals = n_normals;
   sp.deflate = deflate;
+  sp.n_deflate = deflate ? n_deflate : 0;
+  sp.deflate_ld = a.n;  // column-major n x n_deflate (global n in the distributed mode)
   require(cfg.k >= 1, MG_ERR_INPUT, "block size must be >= 1, got " + std::to_string(cfg.k));
   require(cfg.tol > 0, MG_ERR_INPUT, "tolerance must be positive, got " + std::to_string(cfg.tol));
   require(cfg.k <= a.n, MG_ERR_INPUT,
@@ -653,6 +656,22 @@ int mg_lobpcg(mg_ctx *ctx, int64_t n, const int64_t *a_indptr, const int64_t *a_
   MG_API_END
 }
 
+int mg_lobpcg_deflate(mg_ctx *ctx, int64_t n, const int64_t *a_indptr, const int64_t *a_indices,
+                      const double *a_data, const double *b, const mg_solver_cfg *cfg,
+                      const double *normals, int64_t n_normals, const double *deflate,
+                      int32_t n_deflate, double *eigenvectors, mg_solver_out *out) {
+  MG_API_BEGIN(ctx)
+  require(cfg != nullptr, MG_ERR_INPUT, "cfg is NULL");
+  require(n_deflate >= 0 && (n_deflate == 0 || deflate != nullptr), MG_ERR_INPUT,
+          "deflate is NULL with n_deflate > 0");
+  check_b(ctx, b, n);
+  SolverIn a{n, a_indptr, a_indices, a_data, nnz_of(ctx, a_indptr, n)};
+  SolveResult r = run_lobpcg(ctx, a, b, *cfg, normals, n_normals, n_deflate ? deflate : nullptr,
+                             eigenvectors, nullptr, nullptr, n_deflate);
+  fill_out(r, out, cfg->k);
+  MG_API_END
+}
+
 int mg_identity_shift(mg_ctx *ctx, int64_t n, const int64_t *q_indptr, const int64_t *q_indices,
                       const double *q_data, const double *normals, int64_t n_normals,
                       int32_t precision, double *epsilon) {
@@ -958,7 +977,9 @@ int mg_embed_host(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *
                           ctx->stream));
   MG_CUDA(cudaMemcpyAsync(dz.p, normals, n_normals * sizeof(double), cudaMemcpyHostToDevice,
                           ctx->stream));
-  DBuf<double> dP(ctx, n * (int64_t)K), db(ctx, n);
+  // reserved == 1 returns all K+1 pairs (the header's P / eigenvalues sizes)
+  const int64_t ncol = (int64_t)K + (cfg->reserved == 1 ? 1 : 0);
+  DBuf<double> dP(ctx, n * ncol), db(ctx, n);
   int rc = MG_OK;
   std::string msg;
   try {
@@ -969,7 +990,7 @@ int mg_embed_host(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *
     rc = e.code;
     msg = e.what();
   }
-  MG_CUDA(cudaMemcpyAsync(P, dP.p, n * (int64_t)K * sizeof(double), cudaMemcpyDeviceToHost,
+  MG_CUDA(cudaMemcpyAsync(P, dP.p, n * ncol * sizeof(double), cudaMemcpyDeviceToHost,
                           ctx->stream));
   MG_CUDA(cudaMemcpyAsync(b, db.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);

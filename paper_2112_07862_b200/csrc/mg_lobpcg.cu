@@ -905,6 +905,19 @@ struct Lobpcg {
   double anorm = 0, bmax = 0, ydenom = 0;
   int64_t zpos = 0;
   bool have_y = false;
+  // deflation vectors (eigensolver.py:179-184): sp.n_deflate columns, vector j
+  // at sp.deflate + j * sp.deflate_ld; each is loaded into column 3mp in turn
+  // and projected out in the reference's sequential order
+  int ndefl = 0, ycur = -1;
+  std::vector<double> ydenoms;
+  void load_y(int j) {
+    if (ycur == j) return;
+    const int g = grid_for(n, 256, ctx->num_sms * 16);
+    k_set_col<T><<<g, 256, 0, ctx->stream>>>(n, sp.deflate + (int64_t)j * sp.deflate_ld, 0.0,
+                                             S.p, ld, 3 * mp);
+    MG_CHECK_LAUNCH(ctx);
+    ycur = j;
+  }
   // distributed mode: this rank owns global rows [row_base, row_base + n)
   Comm *comm = nullptr;
   const DistPart<T> *dp = nullptr;
@@ -1099,6 +1112,14 @@ struct Lobpcg {
   // project y out of physical columns [c_lo, c_hi) (eigensolver.py:92-99)
   void deflate_cols(int c_lo, int c_hi, int region0, int region_w) {
     if (!have_y || c_hi <= c_lo) return;
+    for (int j = 0; j < ndefl; ++j) {
+      if (!(ydenoms[j] > 0.0)) continue;  // eigensolver.py:95-96: denom <= 0 -> unchanged
+      load_y(j);
+      ydenom = ydenoms[j];
+      deflate_one(c_lo, c_hi, region0, region_w);
+    }
+  }
+  void deflate_one(int c_lo, int c_hi, int region0, int region_w) {
     if (sizeof(T) == 8) {
       // fp64: the reference's own arithmetic order (a Gram tile pass, then the
       // transform), which keeps the deflated eps solve on its trajectory
@@ -1655,14 +1676,16 @@ struct Lobpcg {
       ar(t.p, 1, true);
       d2h_sync(ctx, &bmax, t.p, sizeof(double));
     }
-    have_y = sp.deflate != nullptr;
-    if (have_y) {  // deflation vector y at column 3mp, and y'By
-      k_set_col<T><<<g, 256, 0, ctx->stream>>>(n, sp.deflate, 0.0, S.p, ld, 3 * mp);
-      MG_CHECK_LAUNCH(ctx);
+    ndefl = sp.deflate ? std::max(1, sp.n_deflate) : 0;
+    have_y = ndefl > 0;
+    ydenoms.assign(ndefl, 0.0);
+    for (int j = 0; j < ndefl; ++j) {  // deflation vector y at column 3mp, and y'By
+      load_y(j);
       GramSpec gy = gspec(3 * mp, 1, 3 * mp, 1, 0, 0);
       pass(0, 0, 0, 0, 0, 0, 0, &gy, 1, Gr0.p, nullptr);
-      d2h_sync(ctx, &ydenom, Gr0.p, sizeof(double));
+      d2h_sync(ctx, &ydenoms[j], Gr0.p, sizeof(double));
     }
+    if (ndefl) ydenom = ydenoms[0];
 
     // ---- initial block (eigensolver.py:177-200)
     zpos = 0;

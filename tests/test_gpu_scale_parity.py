@@ -1,0 +1,238 @@
+"""GPU parity against the reference at the benchmarked scales (C3, C4, C5 families).
+
+The goldens (``tests/golden/scale_*.json|npz``) were written by
+``tests/golden/make_golden_scale.py``, which runs the UNMODIFIED reference
+(``manigraph``) in the build container on the same harness graphs.  Here the
+sm_100a path rebuilds each graph, then every operator piece is compared with
+what the reference computed:
+
+* T / L / Q / A structure and values: sha256 equality (bit-exact; A is
+  assembled with the reference's own eps and mu, operators.py:179-186);
+* eps (the 60-iteration best-effort deflated LOBPCG, operators.py:138-156):
+  1e-10 relative in fp64 (SURVEY 8(c) protocol item 2);
+* mu: exact;  b: 1e-13 relative at 8192 sampled rows plus global sums;
+* ``OperatorPair.diagnostics()`` keys equal;
+* C5 family at 200K (K = 32, fp32, tol 1e-4): eigenvalues within the
+  north_star's 1e-4 relative of the reference's own LOBPCG and of the tight
+  (shift-invert) eigenvalues; complete-cluster principal angles within
+  max(1e-3, 2.5 x the reference's own angle) of the tight vectors, plus the
+  a-posteriori (Davis-Kahan) bound per cluster;
+* C4 family at 500K (disconnected, K = 16): the device k-means labels on the
+  row-normalised first 10 columns equal the reference's labels up to
+  permutation (the reference's partition is the 10 patches).
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, principal_angles
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["c5_200K", "c3_1M", "c4_500K", "c5_1M", "c5_2M"]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def load(name):
+    path = os.path.join(GOLDEN, f"scale_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"golden {name} not generated")
+    with open(path) as fh:
+        meta = json.load(fh)
+    z = np.load(os.path.join(GOLDEN, f"scale_{name}.npz"))
+    return z, meta
+
+
+@pytest.fixture(scope="module")
+def mg():
+    import paper_2112_07862_b200 as mg
+    return mg
+
+
+_graphs = {}
+
+
+def graph(name, meta):
+    if name not in _graphs:
+        from paper_2112_07862_b200 import synthetic
+        g = synthetic.config_graph(meta["config"], n=meta["n"])
+        gm = meta["graph"]
+        assert sha(g[1]) == gm["sha_indptr"] and sha(g[2]) == gm["sha_indices"]
+        assert sha(g[3]) == gm["sha_weights"]
+        _graphs.clear()
+        _graphs[name] = g
+    return _graphs[name]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_operator_pair_matches_reference(mg, name):
+    z, meta = load(name)
+    g = graph(name, meta)
+    pm = meta["pair"]
+    G = mg.Graph(*g)
+    l = mg.laplacian(G)
+    assert (sha(l.indptr), sha(l.indices), sha(l.data)) == (
+        pm["sha_L_ptr"], pm["sha_L_idx"], pm["sha_L_val"])
+    t = mg.two_hop_sets(G)
+    assert t.indices.size == pm["T_nnz"]
+    assert sha(t.indptr) == pm["sha_T_ptr"] and sha(t.indices) == pm["sha_T_idx"]
+    q = mg.two_hop_laplacian(t)
+    assert q.nnz == pm["Q_nnz"]
+    assert (sha(q.indptr), sha(q.indices), sha(q.data)) == (
+        pm["sha_Q_ptr"], pm["sha_Q_idx"], pm["sha_Q_val"])
+    eps = mg.identity_shift(q)
+    assert abs(eps - pm["eps"]) <= 1e-10 * abs(pm["eps"]), (eps, pm["eps"])
+    mu = mg.repulsion_weight(l, q, pm["eps"])
+    assert mu == pm["mu"]
+    a = mg.assemble_operator(l, q, pm["mu"], pm["eps"])
+    assert a.nnz == pm["A_nnz"]
+    assert (sha(a.indptr), sha(a.indices), sha(a.data)) == (
+        pm["sha_A_ptr"], pm["sha_A_idx"], pm["sha_A_val"])
+    bs = mg.degree_balancing(a)
+    b = bs.b
+    rows = z["b_rows"]
+    assert np.max(np.abs(b[rows] - z["b_at_rows"]) / z["b_at_rows"]) < 1e-13
+    st = pm["b_stats"]
+    assert abs(np.sum(b) - st["sum"]) <= 1e-12 * abs(st["sum"])
+    assert abs(np.sum(b * b) - st["sumsq"]) <= 1e-12 * abs(st["sumsq"])
+    assert b.min() == pytest.approx(st["min"], rel=1e-13)
+    assert b.max() == pytest.approx(st["max"], rel=1e-13)
+    assert bs.generalized_degree == pytest.approx(pm["generalized_degree"], rel=1e-13)
+    pair = mg.OperatorPair(A=a, B=bs, mu=mu, epsilon=pm["eps"], Q=q)
+    d = pair.diagnostics()
+    rd = pm["diagnostics"]
+    assert set(d) == set(rd)
+    assert d["binding_row"] == rd["binding_row"] and d["q_nnz"] == rd["q_nnz"]
+    assert d["min_disc_left_end"] == pytest.approx(rd["min_disc_left_end"], rel=1e-12, abs=1e-300)
+
+
+def test_c5_200k_eigenpairs_vs_reference(mg):
+    z, meta = load("c5_200K")
+    if "tight" not in meta or "clusters" not in meta:
+        pytest.skip("tight solution not in the golden")
+    from paper_2112_07862_b200 import core
+    g = graph("c5_200K", meta)
+    cfg = mg.SolverConfig(k=33, tol=1e-4, max_iter=3000, seed=42, precision="fp32")
+    res, bt, dg = core.embed_arrays(*g, 32, cfg)
+    assert res.converged.all()
+    ev = res.eigenvalues
+    vecs = res.eigenvectors.cpu().numpy()
+    b = bt.cpu().numpy()
+    tight = z["tight_eigenvalues"][:33]
+    ref = z["ref_eigenvalues"]
+    # north_star: fp32 eigenvalues within 1e-4 relative of the oracle
+    assert np.max(np.abs(ev - ref) / ref) < 1e-4, np.abs(ev - ref) / ref
+    assert np.max(np.abs(ev - tight) / tight) < 1e-4, np.abs(ev - tight) / tight
+    V = z["tight_eigenvectors"].astype(np.float64)
+    pair = mg.build_operator_pair(mg.Graph(*g))
+    A = pair.A
+    lam = z["tight_eigenvalues"]
+    for c, ref_ang in zip(meta["clusters"]["complete"], meta["clusters"]["ref_angle_per_cluster"]):
+        ang = float(principal_angles(vecs[:, c], V[:, c], b).max())
+        assert ang <= max(1e-3, 2.5 * ref_ang), (c, ang, ref_ang)
+        # a-posteriori bound (B inner product): sin angle <= ||R||_{B^-1} / gap
+        X = vecs[:, c]
+        th = np.array([float(X[:, j] @ A.matvec(X[:, j])) / float(X[:, j] @ (b * X[:, j]))
+                       for j in range(len(c))])
+        R = A.matmat(X) - (b[:, None] * X) * th
+        rn = np.sqrt(np.sum(R * R / b[:, None]))
+        others = np.delete(lam, c)
+        gap = np.min(np.abs(others[:, None] - th[None, :]))
+        assert ang <= 1.05 * rn / gap + 1e-6, (c, ang, rn / gap)
+
+
+def test_c5_200k_sign_convention(mg):
+    """Sign convention (eigensolver.py:83-89): the largest-|entry| of every
+    simple (non-degenerate) column is positive, and agrees in sign with the
+    reference-convention tight vector at that row."""
+    z, meta = load("c5_200K")
+    if "clusters" not in meta:
+        pytest.skip("tight solution not in the golden")
+    from paper_2112_07862_b200 import core
+    g = graph("c5_200K", meta)
+    cfg = mg.SolverConfig(k=33, tol=1e-4, max_iter=3000, seed=42, precision="fp32")
+    res, bt, dg = core.embed_arrays(*g, 32, cfg)
+    vecs = res.eigenvectors.cpu().numpy()
+    V = z["tight_eigenvectors"].astype(np.float64)
+    simple = [c[0] for c in meta["clusters"]["complete"] if len(c) == 1]
+    assert simple, "no simple eigenvalue in the block"
+    for j in simple:
+        i = int(np.argmax(np.abs(vecs[:, j])))
+        assert vecs[i, j] > 0
+        assert np.sign(V[i, j]) == 1.0 or abs(V[i, j]) < 1e-3 * np.abs(V[:, j]).max()
+
+
+def test_c4_500k_kmeans_labels_match_reference(mg):
+    z, meta = load("c4_500K")
+    if "solve" not in meta:
+        pytest.skip("reference labels not in the golden")
+    assert meta["solve"]["labels_equal_patches_up_to_permutation"]
+    from paper_2112_07862_b200 import core
+    g = graph("c4_500K", meta)
+    n = g[0]
+    cfg = mg.SolverConfig(k=17, tol=1e-5, max_iter=3000, seed=42, precision="fp32")
+    res, bt, dg = core.embed_arrays(*g, 16, cfg, check_connected=False)
+    assert res.converged.all()
+    x = mg.normalize_rows(res.eigenvectors.cpu().numpy()[:, :10])
+    labels = mg.kmeans(x, 10)
+    ref_first = z["ref_labels_first_per_patch"]
+    # the reference's labels are constant on each patch (checked at generation);
+    # ours must induce the same partition
+    per = n // 10
+    ref_labels = np.repeat(ref_first, per)
+    pairs = set(zip(labels.tolist(), ref_labels.tolist()))
+    assert len(pairs) == len(set(labels.tolist())) == len(set(ref_labels.tolist())) == 10
+
+
+def test_hub_large_row_tier_bit_exact(mg):
+    """Every leaf row of the hub graph has > 512 adj*adj products, so the
+    two-hop builder runs its large-row tier (flag / gather / segmented sort)."""
+    z, meta = load("hub")
+    assert meta["rows_over_512_products"] > 0
+    g = mg.Graph(int(z["graph_n"]), z["graph_ptr"], z["graph_idx"], z["graph_w"])
+    t = mg.two_hop_sets(g)
+    assert np.array_equal(t.indptr, z["T_ptr"]) and np.array_equal(t.indices, z["T_idx"])
+    for lit, key in ((False, "Q"), (True, "QL")):
+        q = mg.two_hop_laplacian(t, literal_diagonal=lit)
+        assert np.array_equal(q.indptr, z[f"{key}_ptr"])
+        assert np.array_equal(q.indices, z[f"{key}_idx"])
+        assert np.array_equal(q.data, z[f"{key}_val"])
+    q = mg.two_hop_laplacian(t)
+    l = mg.laplacian(g)
+    eps = mg.identity_shift(q)
+    assert abs(eps - meta["eps"]) <= 1e-10 * abs(meta["eps"])
+    assert mg.repulsion_weight(l, q, meta["eps"]) == meta["mu"]
+    a = mg.assemble_operator(l, q, meta["mu"], meta["eps"])
+    assert np.array_equal(a.indptr, z["A_ptr"]) and np.array_equal(a.indices, z["A_idx"])
+    assert np.array_equal(a.data, z["A_val"])
+    b = mg.degree_balancing(a).b
+    assert np.max(np.abs(b - z["b"]) / z["b"]) < 1e-14
+
+
+def test_lobpcg_two_deflation_vectors(mg):
+    """lobpcg_smallest(deflate=[y1 y2]) (eigensolver.py:179-184, 239-241):
+    the vectors are projected out one after another, like the reference."""
+    z, meta = load("defl2")
+    n = int(z["graph_n"])
+    g = mg.Graph(n, z["graph_ptr"], z["graph_idx"], z["graph_w"])
+    l = mg.laplacian(g)
+    cfg = mg.SolverConfig(k=4, tol=1e-9, max_iter=1000, seed=42)
+    res = mg.lobpcg_smallest(l, z["b"], cfg, deflate=z["deflate"])
+    assert res.converged.all()
+    assert res.iterations == meta["iterations"]
+    ref = z["eigenvalues"]
+    assert np.max(np.abs(res.eigenvalues - ref) / ref) < 1e-8
+    assert np.max(np.abs(res.eigenvalues - z["dense_eigenvalues"][2:6]) / ref) < 1e-8
+    ang = principal_angles(res.eigenvectors, z["eigenvectors"], z["b"])
+    assert ang.max() < 1e-6
+    # single-column input keeps working and equals the one-vector path
+    res1 = mg.lobpcg_smallest(l, z["b"], cfg, deflate=z["deflate"][:, 0])
+    res2 = mg.lobpcg_smallest(l, z["b"], cfg, deflate=z["deflate"][:, :1])
+    assert np.array_equal(res1.eigenvalues, res2.eigenvalues)
