@@ -31,15 +31,6 @@ struct DevCSR {
   // rounding of A_ij becomes a zero-row-sum perturbation whose effect scales
   // with the eigenvalue instead of ||A|| (A and Q are Laplacian-like).
   const T *rowsum = nullptr;
-  // optional row-block structure for the staged SpMM (mg_spmm.cu): block b =
-  // rows [b*rb, b*rb + rb); its distinct columns ucol[uoff[b] .. uoff[b+1])
-  // (sorted), and per nonzero the 16-bit position of its column in that list.
-  // uoff[b+1] - uoff[b] == 0 for a block too large to index (direct gathers).
-  int rb = 0;
-  int64_t nblk = 0;
-  const int64_t *uoff = nullptr;
-  const int *ucol = nullptr;
-  const uint16_t *lidx = nullptr;
 };
 
 // Owning version (conversion from the reference's int64/f64 CSR).
@@ -49,20 +40,8 @@ struct OwnedCSR {
   DBuf<int> idx;
   DBuf<T> val;
   DBuf<T> rowsum;
-  DBuf<int64_t> uoff;
-  DBuf<int> ucol;
-  DBuf<uint16_t> lidx;
   DevCSR<T> view;
 };
-
-// build the row-block structure of an owned CSR (mg_spmm.cu); no-op when the
-// matrix is too small to benefit
-template <typename T>
-void build_blocked(mg_ctx *ctx, OwnedCSR<T> &A);
-// staged SpMM for 4*VN <= w <= kStagedMaxW (fp32 16..36 columns); returns false
-// when it does not apply (caller falls back to k_spmm)
-template <typename T>
-bool spmm_staged(mg_ctx *ctx, const DevCSR<T> &A, const T *X, int ldx, T *Y, int ldy, int w);
 
 template <typename T>
 void make_solver_csr(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *idx,

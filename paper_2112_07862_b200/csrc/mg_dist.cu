@@ -219,7 +219,6 @@ void build_dist(mg_ctx *ctx, Comm *comm, int64_t n, const int64_t *ptr, const in
   dp.A.view.idx = dp.A.idx.p;
   dp.A.view.val = dp.A.val.p;
   dp.A.view.rowsum = diff ? dp.A.rowsum.p : nullptr;
-  build_blocked<T>(ctx, dp.A);  // local columns are [local | halo]: same staged SpMM
   sync(ctx);
 }
 

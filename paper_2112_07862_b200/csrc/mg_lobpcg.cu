@@ -91,7 +91,6 @@ void make_solver_csr(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *
     MG_CHECK_LAUNCH(ctx);
     out.view.rowsum = out.rowsum.p;
   }
-  build_blocked<T>(ctx, out);
 }
 
 // ------------------------------------------------------------------ SpMM ---
@@ -236,7 +235,6 @@ void spmm(mg_ctx *ctx, const DevCSR<T> &A, const T *X, int ldx, T *Y, int ldy, i
   double bytes = (double)A.nnz * (sizeof(T) + sizeof(int)) + 8.0 * (A.n + 1) +
                  2.0 * sizeof(T) * (double)A.n * w;
   ProfScope ps(ctx, PROF_SPMM, bytes);
-  if (spmm_staged<T>(ctx, A, X, ldx, Y, ldy, w)) return;
   if (A.rowsum)
     k_spmm<T, true><<<grid, 256, 0, ctx->stream>>>(A.n, A.ptr, A.idx, A.val, X, ldx, Y, ldy, L,
                                                    A.rowsum);
@@ -1303,7 +1301,6 @@ struct Lobpcg {
   int fast_global = 0;
   DBuf<double> gpart, tcpart;
   bool use_tc = false;      // fp32 wide blocks: tcgen05 3xTF32 Gram pair (mg_tc.cuh)
-  bool use_tc_upd = false;  // ... and the tcgen05 update + residual
   int64_t fast_steps = 0, fast_fallbacks = 0;
 
   int tk_gram = 32, ns_gram = 3, tk_upd = 32, rt_upd = 8;
@@ -1417,7 +1414,6 @@ struct Lobpcg {
     const int w = 3 * mp;
     gpart.alloc(ctx, (size_t)grid_fast * 2 * w * w);
     use_tc = sizeof(T) == 4 && gram_tc_supported(w) && env_double("MG_TC_GRAM", 1) != 0;
-    use_tc_upd = sizeof(T) == 4 && update_tc_supported(w, mp);
     fast_ok = true;
   }
 
@@ -1496,56 +1492,9 @@ struct Lobpcg {
     ua.wc = Wc.p;
     ua.part = colpart.p;
     int nblk_upd = grid_upd;
-    if constexpr (sizeof(T) == 4) {
-      static int chk = -1;
-      if (chk < 0) chk = (int)env_double("MG_TC_UPD_CHECK", 0);
-      if (chk && use_tc_upd && iter_now % chk == 1) {  // debug: TC update vs CUDA-core update
-        DBuf<T> S2(ctx, n * ld), A2(ctx, n * ld), W2(ctx, n * mp);
-        DBuf<double> p2(ctx, (size_t)ctx->num_sms * 2 * mp);
-        MG_CUDA(cudaMemcpyAsync(S2.p, S.p, n * ld * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
-        MG_CUDA(cudaMemcpyAsync(A2.p, AS.p, n * ld * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
-        const T *pr = sp.jacobi ? prec.p : nullptr;
-        update_tc(ctx, n, ld, w, m, mp, (float *)S2.p, (float *)A2.p, (const float *)bw.p,
-                  (const float *)pr, (const float *)M.p, theta.p, status.p + 5, p2.p,
-                  (float *)W2.p);
-        UpdArgs u2 = ua;
-        u2.part = p2.p;  // scratch partials; the real ones are recomputed below
-        k_update_resid<T, 3, 4><<<grid_upd, kFThreads, upd_smem, ctx->stream>>>(
-            S.p, AS.p, bw.p, pr, M.p, theta.p, u2);
-        // NOTE: S/AS now hold the CUDA-core result; the normal path below runs again on
-        // updated data only when the check is off -- so this iteration keeps the CUDA-core result
-        const int64_t rows = std::min<int64_t>(n, 4096);
-        std::vector<T> h1(rows * ld), h2(rows * ld), g1(rows * ld), g2(rows * ld);
-        d2h_sync(ctx, h1.data(), S.p, rows * ld * sizeof(T));
-        d2h_sync(ctx, h2.data(), S2.p, rows * ld * sizeof(T));
-        d2h_sync(ctx, g1.data(), AS.p, rows * ld * sizeof(T));
-        d2h_sync(ctx, g2.data(), A2.p, rows * ld * sizeof(T));
-        for (int blk = 0; blk < 5; ++blk) {
-          const std::vector<T> &u = blk < 3 ? h1 : g1, &v = blk < 3 ? h2 : g2;
-          const int cb = (blk % 3) * mp;
-          double md = 0, mx = 0;
-          for (int64_t r = 0; r < rows; ++r)
-            for (int c = 0; c < m; ++c) {
-              md = std::max(md, (double)std::fabs(u[r * ld + cb + c] - v[r * ld + cb + c]));
-              mx = std::max(mx, (double)std::fabs(u[r * ld + cb + c]));
-            }
-          fprintf(stderr, "[upd check it=%d] %s max|diff| %.3e max|val| %.3e\n", iter_now,
-                  blk == 0 ? "X" : blk == 1 ? "P" : blk == 2 ? "W" : blk == 3 ? "AX" : "AP", md, mx);
-        }
-        goto upd_checked;
-      }
-    }
     {
       ProfScope ps(ctx, PROF_UPDATE, 2.0 * n * ld * sizeof(T) + 5.0 * n * mp * sizeof(T));
       const T *pr = sp.jacobi ? prec.p : nullptr;
-      if constexpr (sizeof(T) == 4) {
-        if (use_tc_upd) {
-          nblk_upd = update_tc(ctx, n, ld, w, m, mp, (float *)S.p, (float *)AS.p,
-                               (const float *)bw.p, (const float *)pr, (const float *)M.p,
-                               theta.p, status.p + 5, colpart.p, (float *)Wc.p);
-          goto upd_done;
-        }
-      }
       if constexpr (sizeof(T) == 4) {
         if (upd_ws) {
           UpdArgs uw = ua;
@@ -1569,7 +1518,6 @@ struct Lobpcg {
       MG_CHECK_LAUNCH(ctx);
     upd_done:;
     }
-  upd_checked:
     if (dbg_ctrl && (iter_now % 50) == 1) {
       long long clk[32];
       d2h_sync(ctx, clk, scratch.p + clk_off, sizeof(clk));

@@ -31,14 +31,10 @@ def _gram_tc(S, AS, b, w):
     return GB.cpu().numpy().reshape(w, w), GA.cpu().numpy().reshape(w, w)
 
 
-@pytest.mark.parametrize("pieces", ["3", "2"])
 @pytest.mark.parametrize("n,w,ld", [(100_003, 108, 116), (4_099, 68, 72), (37, 100, 104), (50_001, 60, 68),
                                     (1_000_000, 108, 116)])
-def test_gram_pair_tc_vs_fp64(n, w, ld, pieces, monkeypatch):
-    if pieces == "3" and not 64 < w <= 112:
-        pytest.skip("the 3-piece (v1) kernel covers 64 < w <= 112")
-    monkeypatch.setenv("MG_TC_PIECES", pieces)
-    bar = 5e-7 if pieces == "3" else 2e-6
+def test_gram_pair_tc_vs_fp64(n, w, ld):
+    bar = 2e-6
     rng = np.random.default_rng(n)
     S = rng.standard_normal((n, ld)) / np.sqrt(n)
     S[:, :8] *= 40.0          # mixed column scales (X vs W blocks)
