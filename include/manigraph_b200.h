@@ -123,6 +123,24 @@ int mg_degree_balancing(mg_ctx *ctx, int64_t n, const int64_t *a_indptr,
                         const int64_t *a_indices, const double *a_data, double *b /* device n */,
                         double *generalized_degree /* host */, int64_t *isolated_node /* host */);
 
+/* SparseSymMatrix.row_sums (sparse.py:79-82) and Graph.degrees
+ * (graph.py:93-96): per-row sums in stored order; out device n. */
+int mg_row_sums(mg_ctx *ctx, int64_t n, const int64_t *indptr, const double *data, double *out);
+
+/* SparseSymMatrix.gershgorin / disc_left_ends (sparse.py:84-98): centers =
+ * stored diagonal, radii = off-diagonal |a_ij| summed in stored order, left
+ * ends = centers - radii; each output device n, or NULL to skip. */
+int mg_gershgorin(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                  const double *data, double *centers, double *radii, double *left_ends);
+
+/* SparseSymMatrix.frobenius_norm (sparse.py:76-77): sqrt of numpy's pairwise
+ * sum of the squared values, bit for bit; out host. */
+int mg_frobenius_norm(mg_ctx *ctx, int64_t nnz, const double *data, double *out);
+
+/* balance_radii (operators.py:189-202): b device n, generalized_degree host. */
+int mg_balance_radii(mg_ctx *ctx, int64_t n, const double *radii, double *b,
+                     double *generalized_degree);
+
 /* OperatorPair.diagnostics (operators.py:76-85): min disc left end + row. */
 int mg_disc_left_min(mg_ctx *ctx, int64_t n, const int64_t *a_indptr, const int64_t *a_indices,
                      const double *a_data, double *min_left /* host */,

@@ -18,6 +18,7 @@ from .core import (  # noqa: F401
     SparseSymMatrix,
     TwoHopSets,
     assemble_operator,
+    balance_radii,
     build_operator_pair,
     connected_components,
     degree_balancing,

@@ -72,6 +72,10 @@ SIGNATURES = {
     "mg_assemble_fill": [vp, i64, vp, vp, vp, vp, vp, vp, f64, f64, vp, vp, vp],
     "mg_degree_balancing": [vp, i64, vp, vp, vp, vp, P_f64, P_i64],
     "mg_disc_left_min": [vp, i64, vp, vp, vp, P_f64, P_i64],
+    "mg_row_sums": [vp, i64, vp, vp, vp],
+    "mg_gershgorin": [vp, i64, vp, vp, vp, vp, vp, vp],
+    "mg_frobenius_norm": [vp, i64, vp, P_f64],
+    "mg_balance_radii": [vp, i64, vp, vp, P_f64],
     "mg_lobpcg": [vp, i64, vp, vp, vp, vp, C.POINTER(SolverCfg), vp, i64, vp, vp,
                   C.POINTER(SolverOut)],
     "mg_lobpcg_deflate": [vp, i64, vp, vp, vp, vp, C.POINTER(SolverCfg), vp, i64, vp, i32, vp,

@@ -166,12 +166,92 @@ class Graph(_DevCache):
     def from_csr(cls, n, indptr, indices, weights):
         return cls(n, indptr, indices, weights)
 
+    @classmethod
+    def from_edges(cls, edges, n: int | None = None) -> "Graph":
+        """graph.py:31-79: ``(i, j)`` / ``(i, j, w)`` tuples (or an (E, 2|3)
+        array) -> canonical CSR.  Same validation and messages as the reference
+        (first offending edge in input order); vectorised host preprocessing."""
+        arr = edges if isinstance(edges, np.ndarray) else list(edges)
+        if isinstance(arr, list):
+            if not arr:
+                ii = jj = np.zeros(0, np.int64)
+                ww = np.zeros(0)
+            else:
+                w3 = [e if len(e) == 3 else (e[0], e[1], 1.0) for e in arr]
+                ii = np.array([int(e[0]) for e in w3], np.int64)
+                jj = np.array([int(e[1]) for e in w3], np.int64)
+                ww = np.array([float(e[2]) for e in w3], np.float64)
+        else:
+            a2 = np.atleast_2d(arr)
+            ii, jj = a2[:, 0].astype(np.int64), a2[:, 1].astype(np.int64)
+            ww = a2[:, 2].astype(np.float64) if a2.shape[1] > 2 else np.ones(len(a2))
+        bad_self = ii == jj
+        bad_neg = (ii < 0) | (jj < 0)
+        bad_w = ~((ww > 0.0) & np.isfinite(ww))
+        first = np.flatnonzero(bad_self | bad_neg | bad_w)
+        if first.size:
+            e = int(first[0])
+            i, j, w = int(ii[e]), int(jj[e]), float(ww[e])
+            if bad_self[e]:
+                raise InputError(f"self-loop on node {i}")
+            if bad_neg[e]:
+                raise InputError(f"negative node id in edge ({i}, {j})")
+            raise InputError(f"edge ({i}, {j}) has non-positive weight {w}")
+        n_implied = int(max(ii.max(initial=-1), jj.max(initial=-1))) + 1
+        if n is None:
+            n = n_implied
+        elif n < n_implied:
+            raise InputError(f"edge references node {n_implied - 1} >= n={n}")
+        n = int(n)
+        lo, hi = np.minimum(ii, jj), np.maximum(ii, jj)
+        key = lo * n + hi
+        uniq, counts = np.unique(key, return_counts=True)
+        if np.any(counts > 1):
+            k = int(uniq[np.argmax(counts > 1)])
+            raise InputError(f"duplicate edge {{{k // n}, {k % n}}}")
+        src = np.concatenate([lo, hi])
+        dst = np.concatenate([hi, lo])
+        wts = np.concatenate([ww, ww])
+        order = np.lexsort((dst, src))
+        src, dst, wts = src[order], dst[order], wts[order]
+        indptr = np.zeros(n + 1, np.int64)
+        np.cumsum(np.bincount(src, minlength=n), out=indptr[1:])
+        return cls(n, indptr, dst, wts)
+
     @property
     def num_edges(self) -> int:
         return int(self.indices.size) // 2
 
     def neighbors(self, i):
         return self.indices[self.indptr[i]:self.indptr[i + 1]]
+
+    def neighbor_weights(self, i):
+        return self.weights[self.indptr[i]:self.indptr[i + 1]]
+
+    def degrees(self):
+        """graph.py:93-96: weighted degrees in neighbor-sorted order (device)."""
+        return _row_sums(self.n, *self._device()[::2])
+
+    def edge_array(self):
+        """graph.py:98-102: each edge once as (i, j, w) with i < j."""
+        rows = np.repeat(np.arange(self.n), np.diff(self.indptr))
+        mask = rows < self.indices
+        return rows[mask], self.indices[mask], self.weights[mask]
+
+    def adjacency(self):
+        """graph.py:104-105."""
+        return SparseSymMatrix(self.n, self.indptr, self.indices, self.weights)
+
+    def __eq__(self, other) -> bool:
+        """graph.py:128-135 (also equal to a reference Graph with the same arrays)."""
+        return (hasattr(other, "indptr") and hasattr(other, "weights")
+                and self.n == int(other.n)
+                and np.array_equal(self.indptr, other.indptr)
+                and np.array_equal(self.indices, other.indices)
+                and np.array_equal(self.weights, other.weights))
+
+    def __hash__(self):
+        return id(self)
 
     def connected_components(self):
         """graph.py:107-123 on the device: (count, labels)."""
@@ -199,6 +279,14 @@ class SparseSymMatrix(_DevCache):
     @classmethod
     def zeros(cls, n):
         return cls(n, np.zeros(n + 1, np.int64), [], [])
+
+    @classmethod
+    def from_scipy(cls, m):
+        """sparse.py:35-38: any scipy sparse matrix -> sorted CSR."""
+        import scipy.sparse as sp
+        m = sp.csr_matrix(m)
+        m.sort_indices()
+        return cls(m.shape[0], m.indptr, m.indices, m.data)
 
     @classmethod
     def from_coo(cls, n, rows, cols, vals):
@@ -239,6 +327,30 @@ class SparseSymMatrix(_DevCache):
 
     def trace(self):
         return float(self.diagonal().sum())
+
+    def frobenius_norm(self) -> float:
+        """sparse.py:76-77 on the device (numpy's pairwise sum, bit for bit)."""
+        out = C.c_double(0)
+        if self.nnz == 0:
+            return 0.0
+        _, _, d = self._device()
+        _sync()
+        _call("mg_frobenius_norm", _ctx(), self.nnz, _ptr(d), C.byref(out))
+        return float(out.value)
+
+    def row_sums(self):
+        """sparse.py:79-82: per-row sums in stored order (device)."""
+        p, _, d = self._device()
+        return _row_sums(self.n, p, d)
+
+    def gershgorin(self):
+        """sparse.py:84-94: (centers, radii) on the device."""
+        c, r, _ = _discs(self, want=(True, True, False))
+        return c, r
+
+    def disc_left_ends(self):
+        """sparse.py:96-98."""
+        return _discs(self, want=(False, False, True))[2]
 
     def matmat(self, X):
         """sparse.py:67-68 on the device (sm_100a SpMM)."""
@@ -375,6 +487,23 @@ class Embedding:
     @property
     def k(self):
         return int(self.P.shape[1])
+
+
+def _row_sums(n, p, d):
+    torch = _t()
+    out = _empty(n, torch.float64)
+    _sync()
+    _call("mg_row_sums", _ctx(), int(n), _ptr(p), _ptr(d), _ptr(out))
+    return _host(out[:n]) if n else np.zeros(0)
+
+
+def _discs(m, want=(True, True, True)):
+    torch = _t()
+    p, i, d = m._device()
+    outs = [_empty(m.n, torch.float64) if w else None for w in want]
+    _sync()
+    _call("mg_gershgorin", _ctx(), m.n, _ptr(p), _ptr(i), _ptr(d), *[_ptr(o) for o in outs])
+    return [(_host(o[:m.n]) if m.n else np.zeros(0)) if o is not None else None for o in outs]
 
 
 def _as_graph(g) -> Graph:
@@ -544,6 +673,20 @@ def assemble_operator(l, q, mu: float, epsilon: float) -> SparseSymMatrix:
     m = SparseSymMatrix(n, _host(ap[:n + 1]), _host(ai[:k]), _host(ad[:k]))
     object.__setattr__(m, "_dcache", (ap[:n + 1], ai[:k], ad[:k]))
     return m
+
+
+def balance_radii(radii) -> DiagonalScaling:
+    """operators.py:189-202: b proportional to radii with unit product (log
+    space, two mean passes, numpy's pairwise means), on the device."""
+    torch = _t()
+    r = np.asarray(radii, dtype=np.float64)
+    n = int(r.size)
+    rd = _dev(r, torch.float64)
+    b = _empty(n, torch.float64)
+    g = C.c_double(0)
+    _sync()
+    _call("mg_balance_radii", _ctx(), n, _ptr(rd), _ptr(b), C.byref(g))
+    return DiagonalScaling(b=_host(b[:n]) if n else np.zeros(0), generalized_degree=float(g.value))
 
 
 def degree_balancing(a) -> DiagonalScaling:

@@ -76,12 +76,9 @@ void dense_eigvals(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *id
   d2h_sync(ctx, w_host, w.p, n * sizeof(double));
 }
 
+// ||A||_F as the reference computes it (sparse.py:76-77: numpy pairwise sum)
 static double frobenius(mg_ctx *ctx, const double *data, int64_t nnz) {
-  if (nnz == 0) return 0.0;
-  DBuf<double> sq(ctx, nnz);
-  k_sq<<<grid_for(nnz, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(data, sq.p, nnz);
-  MG_CHECK_LAUNCH(ctx);
-  return std::sqrt(sum_f64(ctx, sq.p, nnz));
+  return frobenius_np(ctx, data, nnz);
 }
 
 static int64_t nnz_of(mg_ctx *ctx, const int64_t *ptr, int64_t n) {
@@ -633,6 +630,40 @@ int mg_degree_balancing(mg_ctx *ctx, int64_t n, const int64_t *a_indptr,
     throw Error(MG_ERR_DISCONNECTED, "node " + std::to_string(bad) +
                                          " has no off-diagonal coupling; extract the largest "
                                          "connected component and retry");
+  MG_API_END
+}
+
+int mg_row_sums(mg_ctx *ctx, int64_t n, const int64_t *indptr, const double *data,
+                double *out) {
+  MG_API_BEGIN(ctx)
+  require(n >= 0, MG_ERR_INPUT, "n must be non-negative");
+  row_sums(ctx, n, indptr, data, out);
+  sync(ctx);
+  MG_API_END
+}
+
+int mg_gershgorin(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                  const double *data, double *centers, double *radii, double *left_ends) {
+  MG_API_BEGIN(ctx)
+  require(n >= 0, MG_ERR_INPUT, "n must be non-negative");
+  gershgorin(ctx, n, indptr, indices, data, centers, radii, left_ends);
+  sync(ctx);
+  MG_API_END
+}
+
+int mg_frobenius_norm(mg_ctx *ctx, int64_t nnz, const double *data, double *out) {
+  MG_API_BEGIN(ctx)
+  require(nnz >= 0 && out != nullptr, MG_ERR_INPUT, "bad frobenius_norm arguments");
+  *out = frobenius_np(ctx, data, nnz);
+  MG_API_END
+}
+
+int mg_balance_radii(mg_ctx *ctx, int64_t n, const double *radii, double *b,
+                     double *generalized_degree) {
+  MG_API_BEGIN(ctx)
+  require(n >= 0 && generalized_degree != nullptr, MG_ERR_INPUT, "bad balance_radii arguments");
+  balance_radii(ctx, n, radii, b, generalized_degree);
+  sync(ctx);
   MG_API_END
 }
 

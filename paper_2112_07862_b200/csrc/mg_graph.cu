@@ -733,33 +733,13 @@ __global__ void k_radii(int64_t n, const int64_t *__restrict__ ptr, const int64_
   }
 }
 
-__global__ void k_log(const double *__restrict__ x, double *__restrict__ y, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = log(x[i]);
-}
-
-__global__ void k_sub_scalar(double *__restrict__ y, const double *__restrict__ x, double c,
-                             int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = __dsub_rn(x[i], c);
-}
-
-__global__ void k_exp_sub(double *__restrict__ b, const double *__restrict__ x, double c,
-                          int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    b[i] = exp(__dsub_rn(x[i], c));
-}
-
 int64_t degree_balancing(mg_ctx *ctx, int64_t n, const int64_t *aptr, const int64_t *aidx,
                          const double *adata, double *b, double *gdeg, const int64_t *perm) {
   if (n == 0) {
     *gdeg = NAN;
     return -1;
   }
-  DBuf<double> rad(ctx, n), logr(ctx, n);
+  DBuf<double> rad(ctx, n);
   DBuf<unsigned long long> bad(ctx, 1);
   MG_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), ctx->stream));
   int g = grid_for(n, kBlock, ctx->num_sms * 16);
@@ -768,15 +748,8 @@ int64_t degree_balancing(mg_ctx *ctx, int64_t n, const int64_t *aptr, const int6
   unsigned long long first;
   d2h_sync(ctx, &first, bad.p, sizeof(first));
   if (first != ~0ull) return (int64_t)first;
-  k_log<<<g, kBlock, 0, ctx->stream>>>(rad.p, logr.p, n);
-  MG_CHECK_LAUNCH(ctx);
-  double mean1 = sum_f64(ctx, logr.p, n) / (double)n;
-  k_sub_scalar<<<g, kBlock, 0, ctx->stream>>>(rad.p, logr.p, mean1, n);  // rad <- logb
-  MG_CHECK_LAUNCH(ctx);
-  double mean2 = sum_f64(ctx, rad.p, n) / (double)n;
-  k_exp_sub<<<g, kBlock, 0, ctx->stream>>>(b, rad.p, mean2, n);
-  MG_CHECK_LAUNCH(ctx);
-  *gdeg = exp(mean1);
+  // means as numpy's pairwise sums (np.mean), mg_queries.cu
+  balance_radii(ctx, n, rad.p, b, gdeg, perm);
   return -1;
 }
 

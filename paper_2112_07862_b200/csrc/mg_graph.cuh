@@ -48,6 +48,17 @@ void dense_eigvals(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *id
 
 // deterministic fp64 reductions over a device array
 double sum_f64(mg_ctx *ctx, const double *x, int64_t n);
+// numpy's pairwise summation (np.sum of a contiguous float64 array), bit for bit
+double np_sum_f64(mg_ctx *ctx, const double *x, int64_t n);
+// sqrt(np.sum(data * data)) (sparse.py:76-77)
+double frobenius_np(mg_ctx *ctx, const double *data, int64_t nnz);
+// mg_queries.cu: sequential row sums; Gershgorin centers / radii / left ends
+// (any output may be null); balance_radii (operators.py:189-202)
+void row_sums(mg_ctx *ctx, int64_t n, const int64_t *ptr, const double *v, double *out);
+void gershgorin(mg_ctx *ctx, int64_t n, const int64_t *ptr, const int64_t *idx, const double *v,
+                double *center, double *radius, double *left);
+void balance_radii(mg_ctx *ctx, int64_t n, const double *radii, double *b, double *gdeg,
+                   const int64_t *perm = nullptr);
 double max_f64_const(mg_ctx *ctx, const double *x, int64_t n);
 
 }  // namespace mg

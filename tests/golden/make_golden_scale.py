@@ -288,6 +288,46 @@ def make_defl():
     print("defl2", meta, res.eigenvalues, flush=True)
 
 
+def make_queries():
+    """SparseSymMatrix.frobenius_norm / row_sums / gershgorin / disc_left_ends,
+    Graph.degrees / edge_array, balance_radii (sparse.py:76-98, graph.py:93-102,
+    operators.py:189-202) on the reference's own matrices: small graphs in full,
+    the C5-family 200K operator as hashes (its frobenius norm exercises numpy's
+    pairwise-summation tree far past one 128-element block)."""
+    out, meta = {}, {"reference": "manigraph (unmodified)"}
+    cases = {"rand700": synthetic.random_connected(np.random.default_rng(99), 700, extra=900,
+                                                   weighted=True),
+             "grid": synthetic.named("grid", (30, 40)),
+             "c5_200K": synthetic.config_graph("c5", n=200_000)}
+    for name, g in cases.items():
+        G = mg.Graph(*g)
+        l = mg.laplacian(G)
+        q = mg.two_hop_laplacian(mg.two_hop_sets(G))
+        rec = {}
+        for key, m in (("L", l), ("Q", q)):
+            c, r = m.gershgorin()
+            rec[key] = {"frobenius_norm": m.frobenius_norm(), "sha_row_sums": sha(m.row_sums()),
+                        "sha_centers": sha(c), "sha_radii": sha(r),
+                        "sha_left": sha(m.disc_left_ends()), "trace": m.trace()}
+            bs = mg.operators.balance_radii(r)
+            rec[key]["balance_b_sum"] = float(np.sum(bs.b))
+            rec[key]["balance_gdeg"] = float(bs.generalized_degree)
+            if g[0] <= 5000:
+                out[f"{name}/{key}_row_sums"] = m.row_sums()
+                out[f"{name}/{key}_radii"] = r
+                out[f"{name}/{key}_left"] = m.disc_left_ends()
+                out[f"{name}/{key}_balance_b"] = bs.b
+        rec["sha_degrees"] = sha(G.degrees())
+        rec["num_edges"] = G.num_edges
+        if g[0] <= 5000:
+            out[f"{name}/degrees"] = G.degrees()
+            out[f"{name}/graph_ptr"], out[f"{name}/graph_idx"], out[f"{name}/graph_w"] = g[1], g[2], g[3]
+            out[f"{name}/graph_n"] = np.int64(g[0])
+        meta[name] = rec
+    save("queries", out, meta)
+    print("queries", json.dumps(meta)[:400], flush=True)
+
+
 def save(name, out, meta):
     np.savez_compressed(os.path.join(HERE, f"scale_{name}.npz"), **out)
     with open(os.path.join(HERE, f"scale_{name}.json"), "w") as fh:
@@ -300,5 +340,7 @@ if __name__ == "__main__":
             make_hub()
         elif what == "defl2":
             make_defl()
+        elif what == "queries":
+            make_queries()
         else:
             make_case(what)
