@@ -383,8 +383,11 @@ def _signs(vecs):
 
 
 def lobpcg(a: CSR, b, k, tol=1e-8, max_iter=500, seed=42, preconditioner="jacobi",
-           deflate=None, x0=None):
-    """eigensolver.py:156-283.  Returns a dict with the EigenResult fields."""
+           deflate=None, x0=None, iter_times=None):
+    """eigensolver.py:156-283.  Returns a dict with the EigenResult fields.
+    ``iter_times`` (a list, optional) receives the wall time of every
+    iteration of the main loop (bench.py's CPU baseline)."""
+    import time as _time
     n = a.n
     b = np.asarray(b, np.float64)
     if b.shape != (n,):
@@ -440,6 +443,7 @@ def lobpcg(a: CSR, b, k, tol=1e-8, max_iter=500, seed=42, preconditioner="jacobi
     history = []
     it = 0
     for it in range(1, max_iter + 1):
+        t_it = _time.perf_counter()
         R, rn, conv = resid(X, AX, theta)
         history.append(float(theta.sum()))
         if conv.all():
@@ -472,6 +476,8 @@ def lobpcg(a: CSR, b, k, tol=1e-8, max_iter=500, seed=42, preconditioner="jacobi
             theta, Y = ritz(X, AX)
             X, AX = X @ Y, AX @ Y
             P = AP = None
+        if iter_times is not None:
+            iter_times.append(_time.perf_counter() - t_it)
 
     AX = a.matmat(X)
     g = X.T @ AX
