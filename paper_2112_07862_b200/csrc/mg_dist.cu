@@ -158,6 +158,16 @@ __global__ void k_local_csr(int64_t nloc, int64_t r0, const int64_t *__restrict_
   }
 }
 
+__global__ void k_row_has_halo(int64_t nloc, const int64_t *__restrict__ lptr,
+                               const int *__restrict__ lidx, int *__restrict__ flag) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nloc;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int f = 0;
+    for (int64_t k = lptr[r]; k < lptr[r + 1]; ++k) f |= lidx[k] >= nloc;
+    flag[r] = f;
+  }
+}
+
 template <typename T>
 void build_dist(mg_ctx *ctx, Comm *comm, int64_t n, const int64_t *ptr, const int64_t *idx,
                 const double *val, DistPart<T> &dp) {
@@ -219,6 +229,27 @@ void build_dist(mg_ctx *ctx, Comm *comm, int64_t n, const int64_t *ptr, const in
   dp.A.view.idx = dp.A.idx.p;
   dp.A.view.val = dp.A.val.p;
   dp.A.view.rowsum = diff ? dp.A.rowsum.p : nullptr;
+  // interior / boundary row lists (ascending local ids)
+  std::vector<int> ri, rb;
+  if (dp.nloc > 0) {
+    DBuf<int> flag(ctx, dp.nloc);
+    k_row_has_halo<<<grid_for(dp.nloc, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+        dp.nloc, dp.A.ptr.p, dp.A.idx.p, flag.p);
+    MG_CHECK_LAUNCH(ctx);
+    std::vector<int> fh(dp.nloc);
+    d2h_sync(ctx, fh.data(), flag.p, dp.nloc * sizeof(int));
+    for (int64_t r = 0; r < dp.nloc; ++r) (fh[r] ? rb : ri).push_back((int)r);
+  }
+  dp.n_int = (int64_t)ri.size();
+  dp.n_bnd = (int64_t)rb.size();
+  dp.rows_int.alloc(ctx, std::max<int64_t>(dp.n_int, 1));
+  dp.rows_bnd.alloc(ctx, std::max<int64_t>(dp.n_bnd, 1));
+  if (dp.n_int)
+    MG_CUDA(cudaMemcpyAsync(dp.rows_int.p, ri.data(), dp.n_int * sizeof(int),
+                            cudaMemcpyHostToDevice, ctx->stream));
+  if (dp.n_bnd)
+    MG_CUDA(cudaMemcpyAsync(dp.rows_bnd.p, rb.data(), dp.n_bnd * sizeof(int),
+                            cudaMemcpyHostToDevice, ctx->stream));
   sync(ctx);
 }
 

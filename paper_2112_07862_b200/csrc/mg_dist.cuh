@@ -18,6 +18,10 @@ struct DistPart {
   int64_t nsend = 0;
   DBuf<int> send_rows;            // local row ids to pack, grouped by peer
   OwnedCSR<T> A;                  // local rows, columns in [local | halo] numbering
+  // local rows whose SpMM reads no halo row (interior) / some halo row
+  // (boundary): the interior rows are formed while the halo exchange runs
+  DBuf<int> rows_int, rows_bnd;
+  int64_t n_int = 0, n_bnd = 0;
 };
 
 // halo plan from the sorted remote-column lists of every rank (host): the

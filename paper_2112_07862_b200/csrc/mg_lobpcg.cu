@@ -148,7 +148,7 @@ template <typename T, bool DIFF>
 __global__ void __launch_bounds__(256)
     k_spmm(int64_t n, const int64_t *__restrict__ ptr, const int *__restrict__ idx,
            const T *__restrict__ val, const T *__restrict__ X, int ldx, T *__restrict__ Y, int ldy,
-           int L, const T *__restrict__ rowsum) {
+           int L, const T *__restrict__ rowsum, const int *__restrict__ rows) {
   using V = typename VecT<T>::V;
   constexpr int VN = VecT<T>::N;
   int lane = threadIdx.x & 31;
@@ -161,7 +161,10 @@ __global__ void __launch_bounds__(256)
   const uint64_t pf = l2_policy_normal(), pl = l2_policy_last();
   int64_t per_block = (int64_t)(blockDim.x >> 5) * G;
   int64_t stride = (int64_t)gridDim.x * per_block;
-  for (int64_t row = blockIdx.x * per_block + (threadIdx.x >> 5) * G + g; row < n; row += stride) {
+  // rows != null: the i-th row formed is rows[i] (i < n), e.g. the interior
+  // rows of a distributed solve while its halo exchange is in flight
+  for (int64_t ri = blockIdx.x * per_block + (threadIdx.x >> 5) * G + g; ri < n; ri += stride) {
+    const int64_t row = rows ? (int64_t)rows[ri] : ri;
     int64_t s = ptr[row], e = ptr[row + 1];
     T acc[VN], xi[VN];
 #pragma unroll
@@ -224,6 +227,28 @@ __global__ void __launch_bounds__(256)
 }
 
 template <typename T>
+void spmm_rows(mg_ctx *ctx, const DevCSR<T> &A, const T *X, int ldx, T *Y, int ldy, int w,
+               const int *rows, int64_t nrows) {
+  constexpr int VN = VecT<T>::N;
+  int L = w / VN;
+  require(L >= 1 && L <= 32 && w % VN == 0, MG_ERR_INTERNAL, "spmm width");
+  if (nrows <= 0) return;
+  int G = 32 / L;
+  int64_t rows_per_block = 8 * G;
+  int grid = grid_for(nrows, (int)rows_per_block, ctx->num_sms * 64);
+  double bytes = (double)A.nnz * (sizeof(T) + sizeof(int)) * ((double)nrows / std::max<int64_t>(A.n, 1)) +
+                 8.0 * (nrows + 1) + 2.0 * sizeof(T) * (double)nrows * w;
+  ProfScope ps(ctx, PROF_SPMM, bytes);
+  if (A.rowsum)
+    k_spmm<T, true><<<grid, 256, 0, ctx->stream>>>(nrows, A.ptr, A.idx, A.val, X, ldx, Y, ldy, L,
+                                                   A.rowsum, rows);
+  else
+    k_spmm<T, false><<<grid, 256, 0, ctx->stream>>>(nrows, A.ptr, A.idx, A.val, X, ldx, Y, ldy, L,
+                                                    nullptr, rows);
+  MG_CHECK_LAUNCH(ctx);
+}
+
+template <typename T>
 void spmm(mg_ctx *ctx, const DevCSR<T> &A, const T *X, int ldx, T *Y, int ldy, int w) {
   constexpr int VN = VecT<T>::N;
   int L = w / VN;
@@ -237,10 +262,10 @@ void spmm(mg_ctx *ctx, const DevCSR<T> &A, const T *X, int ldx, T *Y, int ldy, i
   ProfScope ps(ctx, PROF_SPMM, bytes);
   if (A.rowsum)
     k_spmm<T, true><<<grid, 256, 0, ctx->stream>>>(A.n, A.ptr, A.idx, A.val, X, ldx, Y, ldy, L,
-                                                   A.rowsum);
+                                                   A.rowsum, nullptr);
   else
     k_spmm<T, false><<<grid, 256, 0, ctx->stream>>>(A.n, A.ptr, A.idx, A.val, X, ldx, Y, ldy, L,
-                                                    nullptr);
+                                                    nullptr, nullptr);
   MG_CHECK_LAUNCH(ctx);
 }
 
@@ -466,6 +491,34 @@ __global__ void k_write_vectors(int64_t n, const T *__restrict__ S, int ld, int 
     int j = (int)(e - r * k);
     int64_t o = perm ? perm[row_base + r] : row_base + r;
     out[o * k + j] = sign[j] * (double)S[r * ld + cols[j]];
+  }
+}
+
+// rows of the selected, sign-fixed columns in storage precision (the
+// distributed gather moves T, not fp64)
+template <typename T>
+__global__ void k_pack_vectors(int64_t n, const T *__restrict__ S, int ld, int k,
+                               const int *__restrict__ cols, const double *__restrict__ sign,
+                               T *__restrict__ out) {
+  int64_t total = n * (int64_t)k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / k;
+    int j = (int)(e - r * k);
+    out[e] = sign[j] < 0.0 ? -S[r * ld + cols[j]] : S[r * ld + cols[j]];
+  }
+}
+
+// gathered solver-order rows -> caller's order (fp64)
+template <typename T>
+__global__ void k_unpack_vectors(int64_t n, int k, const T *__restrict__ in,
+                                 const int64_t *__restrict__ perm, double *__restrict__ out) {
+  int64_t total = n * (int64_t)k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / k;
+    int j = (int)(e - r * k);
+    out[(perm ? perm[r] : r) * k + j] = (double)in[e];
   }
 }
 
@@ -1026,8 +1079,63 @@ struct Lobpcg {
                    sizeof(T));
   }
 
+  // Distributed SpMM of a compact block X (n local rows, then the halo rows,
+  // width wx) over its columns [c0, c0 + w): pack the rows peers need, form
+  // the interior rows (no halo column) while the grouped send/recv runs on the
+  // communication stream, then the boundary rows once the halo has arrived.
+  // MG_HALO_OVERLAP=0 serialises (exchange, then every row).
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+  void halo_spmm(T *X, int wx, int c0, int w, T *dst, int ldd) {
+    static const bool overlap = env_double("MG_HALO_OVERLAP", 1) != 0;
+    if (!overlap) {
+      halo(X, wx);
+      spmm<T>(ctx, A, X + c0, wx, dst, ldd, w);
+      return;
+    }
+    if (!cstream) {
+      MG_CUDA(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+      MG_CUDA(cudaEventCreateWithFlags(&ev_pack, cudaEventDisableTiming));
+      MG_CUDA(cudaEventCreateWithFlags(&ev_halo, cudaEventDisableTiming));
+    }
+    if (dp->nsend > 0) {
+      k_pack_rows<T><<<grid_for(dp->nsend * wx, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+          X, wx, dp->send_rows.p, dp->nsend, sendbuf.p);
+      MG_CHECK_LAUNCH(ctx);
+    }
+    MG_CUDA(cudaEventRecord(ev_pack, ctx->stream));
+    spmm_rows<T>(ctx, A, X + c0, wx, dst, ldd, w, dp->rows_int.p, dp->n_int);
+    MG_CUDA(cudaStreamWaitEvent(cstream, ev_pack, 0));
+    std::vector<int64_t> so(dp->soff), sc(dp->scnt), ro(dp->roff), rc(dp->rcnt);
+    for (size_t p = 0; p < so.size(); ++p) {
+      so[p] *= wx;
+      sc[p] *= wx;
+      ro[p] *= wx;
+      rc[p] *= wx;
+    }
+    mg_ctx cctx;
+    cctx.device = ctx->device;
+    cctx.stream = cstream;
+    cctx.num_sms = ctx->num_sms;
+    comm->exchange(&cctx, sendbuf.p, so.data(), sc.data(), X + (size_t)n * wx, ro.data(),
+                   rc.data(), sizeof(T));
+    MG_CUDA(cudaEventRecord(ev_halo, cstream));
+    MG_CUDA(cudaStreamWaitEvent(ctx->stream, ev_halo, 0));
+    spmm_rows<T>(ctx, A, X + c0, wx, dst, ldd, w, dp->rows_bnd.p, dp->n_bnd);
+  }
+  void release_comm_stream() {
+    if (cstream) {
+      cudaStreamSynchronize(cstream);
+      cudaEventDestroy(ev_pack);
+      cudaEventDestroy(ev_halo);
+      cudaStreamDestroy(cstream);
+      cstream = nullptr;
+    }
+  }
+  ~Lobpcg() { release_comm_stream(); }
+
   // dst = A * src[:, c0:c0+w]; in distributed mode the block is staged
-  // compactly and its halo rows are exchanged first
+  // compactly and its halo rows are exchanged (overlapped with the interior rows)
   void spmm_into(const T *src, int lds, int c0, int w, T *dst, int ldd) {
     if (!comm) {
       spmm<T>(ctx, A, src + c0, lds, dst, ldd, w);
@@ -1036,8 +1144,7 @@ struct Lobpcg {
     k_copy_cols<T><<<grid_for(n * w, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
         n, src, lds, c0, Xe.p, w, 0, w);
     MG_CHECK_LAUNCH(ctx);
-    halo(Xe.p, w);
-    spmm<T>(ctx, A, Xe.p, w, dst, ldd, w);
+    halo_spmm(Xe.p, w, 0, w, dst, ldd);
   }
 
   GramSpec gspec(int r0, int rw, int c0, int cw, int sym, int use_as) {
@@ -1688,7 +1795,6 @@ struct Lobpcg {
         // with one wide SpMM at every full re-orthonormalisation
         spmm_cols(0, 3 * mp);
       } else {
-        halo(Wc.p, mp);
         // soft locking (eigensolver.py:235-238): only active columns of W enter
         // the basis; they usually form a suffix (the smallest pairs converge
         // first), so A W is formed for the 16-byte-aligned column range that
@@ -1700,7 +1806,10 @@ struct Lobpcg {
             break;
           }
         c0 = c0 / VN * VN;
-        spmm<T>(ctx, A, Wc.p + c0, mp, AS.p + 2 * mp + c0, ld, mp - c0);
+        if (comm)
+          halo_spmm(Wc.p, mp, c0, mp - c0, AS.p + 2 * mp + c0, ld);
+        else
+          spmm<T>(ctx, A, Wc.p + c0, mp, AS.p + 2 * mp + c0, ld, mp - c0);
         debug_check("spmm");
       }
       for (int c = 0; c < pcount; ++c) vcols.push_back(mp + c);
@@ -1843,12 +1952,31 @@ struct Lobpcg {
                             ctx->stream));
     MG_CUDA(cudaMemcpyAsync(dcols.p, cols.data(), m * sizeof(int), cudaMemcpyHostToDevice,
                             ctx->stream));
-    if (comm)  // every rank writes its rows of the full block; the sum gathers it
-      MG_CUDA(cudaMemsetAsync(eigvecs, 0, (size_t)n_global * m * sizeof(double), ctx->stream));
-    k_write_vectors<T><<<grid_for(n * m, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-        n, S.p, ld, m, dcols.p, dsign.p, sp.perm, eigvecs, sp.row_base);
-    MG_CHECK_LAUNCH(ctx);
-    ar(eigvecs, (size_t)n_global * m);
+    if (!comm) {
+      k_write_vectors<T><<<grid_for(n * m, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          n, S.p, ld, m, dcols.p, dsign.p, sp.perm, eigvecs, sp.row_base);
+      MG_CHECK_LAUNCH(ctx);
+    } else {
+      // allgather of every rank's rows in storage precision (T): one grouped
+      // send/recv of n_loc x m per peer instead of an fp64 allreduce of the
+      // zero-filled n x m block (2.6 GB instead of 2 x 5.3 GB at C5, fp32)
+      DBuf<T> all(ctx, (size_t)n_global * m);
+      const std::vector<int64_t> &rs = dp->rs;
+      k_pack_vectors<T><<<grid_for(n * m, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          n, S.p, ld, m, dcols.p, dsign.p, all.p + (size_t)sp.row_base * m);
+      MG_CHECK_LAUNCH(ctx);
+      const int R = comm->nranks;
+      std::vector<int64_t> soff(R, sp.row_base * m), scnt(R, n * m), roff(R), rcnt(R);
+      for (int q = 0; q < R; ++q) {
+        roff[q] = rs[q] * m;
+        rcnt[q] = (rs[q + 1] - rs[q]) * m;
+      }
+      comm->exchange(ctx, all.p, soff.data(), scnt.data(), all.p, roff.data(), rcnt.data(),
+                     sizeof(T));
+      k_unpack_vectors<T><<<grid_for(n_global * m, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          n_global, m, all.p, sp.perm, eigvecs);
+      MG_CHECK_LAUNCH(ctx);
+    }
     sync(ctx);
     res.normals_used = zpos;
     res.fast_steps = fast_steps;
