@@ -56,7 +56,32 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_loop(self):
+        """In-process NVML queries (no nvidia-smi process per sample: spawning one
+        every 0.2 s competed with the host-side syncs of the setup stages)."""
+        import pynvml as nv
+        nv.nvmlInit()
+        try:
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(sm), str(smax), f"{pw:.1f}", hex(rs)] +
+                                    ["Active" if rs & b else "Not Active" for b in bits])
+                self._stop.wait(0.2)
+        finally:
+            nv.nvmlShutdown()
+
     def _run(self):
+        try:
+            self._nvml_loop()
+            return
+        except Exception:
+            self.samples = []
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
