@@ -15,12 +15,19 @@
 //   w      = exp(-d2 / sigma2)  (exp within 1 ulp of numpy's), or 1
 //   from_edges: every w must be finite and > 0, CSR of both half-edges sorted
 //            by (row, column).
-// Cost O(n^2 d) like the reference (which is O(n^2) in memory as well); the
-// configs' large graphs come from synthetic.py's tree-based harness instead.
+// Search (round 2): for d <= 3 and n >= 4096 a uniform cell grid (about two
+// points per cell, points bucketed by a radix sort of their cell ids) replaces
+// the all-pairs scan.  Each query visits Chebyshev shells of cells around its
+// own until its k-th candidate is closer than anything outside the visited
+// box can be (true distance bound minus a rounding margin for the reference's
+// sq_i + sq_j - 2 x.x form), so the top-k lists -- compared as (d2, index)
+// pairs, i.e. ties to the lower index -- are exactly the all-pairs ones.
+// Small n, larger d or non-finite inputs keep the exact O(n^2 d) scan.
 #include <cub/cub.cuh>
 #include <vector>
 
 #include "mg_common.cuh"
+#include "mg_graph.cuh"
 #include "mg_knn.cuh"
 
 namespace mg {
@@ -101,6 +108,248 @@ __global__ void __launch_bounds__(kKnnThreads)
     for (int t = 0; t < k; ++t) nbr[i * k + t] = bj[t];
 }
 
+// ------------------------------------------------------------- grid search ---
+constexpr int kGridMaxD = 3;
+
+struct GridSpec {
+  int d;
+  int64_t G[kGridMaxD];   // cells per dimension
+  double lo[kGridMaxD], h[kGridMaxD];
+  double sqmax;
+};
+
+__device__ __forceinline__ int64_t cell_coord(double x, int q, const GridSpec &gs) {
+  int64_t c = (int64_t)floor((x - gs.lo[q]) / gs.h[q]);
+  return c < 0 ? 0 : (c >= gs.G[q] ? gs.G[q] - 1 : c);
+}
+
+__global__ void k_bbox(int64_t n, int d, const double *__restrict__ X, double *__restrict__ part) {
+  // part[block][2d]: min then max per dimension; also flags non-finite values (NaN -> min)
+  __shared__ double smin[kGridMaxD][256], smax[kGridMaxD][256];
+  double mn[kGridMaxD], mx[kGridMaxD];
+  for (int q = 0; q < d; ++q) {
+    mn[q] = INFINITY;
+    mx[q] = -INFINITY;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int q = 0; q < d; ++q) {
+      const double v = X[i * d + q];
+      if (!isfinite(v)) mn[q] = NAN;
+      if (!(v >= mn[q])) mn[q] = isnan(mn[q]) ? mn[q] : v;
+      if (v > mx[q]) mx[q] = v;
+    }
+  for (int q = 0; q < d; ++q) {
+    smin[q][threadIdx.x] = mn[q];
+    smax[q][threadIdx.x] = mx[q];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 0; q < d; ++q) {
+      double a = INFINITY, b = -INFINITY;
+      for (int t = 0; t < (int)blockDim.x; ++t) {
+        const double u = smin[q][t];
+        if (isnan(u) || isnan(a)) a = NAN;
+        else a = fmin(a, u);
+        b = fmax(b, smax[q][t]);
+      }
+      part[blockIdx.x * 2 * d + q] = a;
+      part[blockIdx.x * 2 * d + d + q] = b;
+    }
+}
+
+__global__ void k_cells(int64_t n, GridSpec gs, const double *__restrict__ X,
+                        int64_t *__restrict__ cell, int64_t *__restrict__ id) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = 0;
+    for (int q = gs.d - 1; q >= 0; --q) c = c * gs.G[q] + cell_coord(X[i * gs.d + q], q, gs);
+    cell[i] = c;
+    id[i] = i;
+  }
+}
+
+// start[c] = first sorted position of cell c (start[ncells] = n)
+__global__ void k_cell_starts(int64_t n, int64_t ncells, const int64_t *__restrict__ cell,
+                              int64_t *__restrict__ start) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = cell[p], cp = p ? cell[p - 1] : -1;
+    for (int64_t q = cp + 1; q <= c; ++q) start[q] = p;
+    if (p == n - 1)
+      for (int64_t q = c + 1; q <= ncells; ++q) start[q] = n;
+  }
+}
+
+__global__ void k_gather_sorted(int64_t n, int d, const int64_t *__restrict__ id,
+                                const double *__restrict__ X, const double *__restrict__ sq,
+                                double *__restrict__ Xs, double *__restrict__ sqs) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = id[p];
+    for (int q = 0; q < d; ++q) Xs[p * d + q] = X[i * d + q];
+    sqs[p] = sq[i];
+  }
+}
+
+// one thread per query (queries in cell order for locality)
+template <int D>
+__global__ void __launch_bounds__(128)
+    k_knn_grid(int64_t n, int k, GridSpec gs, const int64_t *__restrict__ id,
+               const double *__restrict__ Xs, const double *__restrict__ sqs,
+               const int64_t *__restrict__ start, int64_t *__restrict__ nbr) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int64_t i = id[p];
+  double xi[D];
+  for (int q = 0; q < D; ++q) xi[q] = Xs[p * D + q];
+  const double sqi = sqs[p];
+  int64_t ci[D];
+  for (int q = 0; q < D; ++q) ci[q] = cell_coord(xi[q], q, gs);
+  double bd[kKnnMaxK];
+  int64_t bj[kKnnMaxK];
+  int cnt = 0;
+  // rounding margin of d2 = (sq_i + sq_j) - 2 x_i.x_j against the true squared distance
+  const double tol = 64.0 * 2.220446049250313e-16 * (sqi + gs.sqmax + 2.0 * sqrt(sqi * gs.sqmax)) +
+                     1e-300;
+  int64_t gmax = 0;
+  for (int q = 0; q < D; ++q) gmax = max(gmax, gs.G[q]);
+  for (int64_t r = 0; r <= gmax; ++r) {
+    // cells with Chebyshev distance exactly r from ci, clipped to the grid
+    int64_t lo[D], hi[D];
+    for (int q = 0; q < D; ++q) {
+      lo[q] = max((int64_t)0, ci[q] - r);
+      hi[q] = min(gs.G[q] - 1, ci[q] + r);
+    }
+    int64_t c[D];
+    for (int q = 0; q < D; ++q) c[q] = lo[q];
+    while (true) {
+      bool shell = false;
+      for (int q = 0; q < D; ++q) shell |= (c[q] == ci[q] - r) || (c[q] == ci[q] + r);
+      if (shell) {
+        int64_t lin = 0;
+        for (int q = D - 1; q >= 0; --q) lin = lin * gs.G[q] + c[q];
+        for (int64_t pp = start[lin]; pp < start[lin + 1]; ++pp) {
+          const int64_t j = id[pp];
+          if (j == i) continue;
+          const double v = pair_d2(xi, Xs + pp * D, D, sqi, sqs[pp]);
+          if (cnt < k) {
+            int t = cnt++;
+            while (t > 0 && (v < bd[t - 1] || (v == bd[t - 1] && j < bj[t - 1]))) {
+              bd[t] = bd[t - 1];
+              bj[t] = bj[t - 1];
+              --t;
+            }
+            bd[t] = v;
+            bj[t] = j;
+          } else if (v < bd[k - 1] || (v == bd[k - 1] && j < bj[k - 1])) {
+            int t = k - 1;
+            while (t > 0 && (v < bd[t - 1] || (v == bd[t - 1] && j < bj[t - 1]))) {
+              bd[t] = bd[t - 1];
+              bj[t] = bj[t - 1];
+              --t;
+            }
+            bd[t] = v;
+            bj[t] = j;
+          }
+        }
+      }
+      int q = 0;
+      for (; q < D; ++q) {
+        if (c[q] < hi[q]) {
+          ++c[q];
+          break;
+        }
+        c[q] = lo[q];
+      }
+      if (q == D) break;
+    }
+    // everything not yet visited lies outside the box of cells within r of ci:
+    // true distance >= the gap from xi to that box's faces (domain edges excluded)
+    double safe = INFINITY;
+    bool all = true;
+    for (int q = 0; q < D; ++q) {
+      if (ci[q] - r > 0) {
+        safe = fmin(safe, (xi[q] - gs.lo[q]) - (double)(ci[q] - r) * gs.h[q]);
+        all = false;
+      }
+      if (ci[q] + r < gs.G[q] - 1) {
+        safe = fmin(safe, (double)(ci[q] + r + 1) * gs.h[q] - (xi[q] - gs.lo[q]));
+        all = false;
+      }
+    }
+    if (all) break;
+    if (cnt == k && safe > 0.0 && bd[k - 1] < safe * safe - tol) break;
+  }
+  for (int t = 0; t < k; ++t) nbr[i * k + t] = t < cnt ? bj[t] : i;
+}
+
+// true: nbr filled by the grid search; false: not applicable (caller scans all pairs)
+bool knn_topk_grid(mg_ctx *ctx, int64_t n, int d, const double *X, const double *sq, int k,
+                   int64_t *nbr) {
+  const char *env = getenv("MG_KNN_GRID");
+  if (env && env[0] == '0') return false;
+  if (d < 1 || d > kGridMaxD || n < 4096) return false;
+  cudaStream_t st = ctx->stream;
+  const int nb = 148;
+  DBuf<double> part(ctx, (size_t)nb * 2 * d);
+  k_bbox<<<nb, 256, 0, st>>>(n, d, X, part.p);
+  MG_CHECK_LAUNCH(ctx);
+  std::vector<double> hp((size_t)nb * 2 * d);
+  d2h_sync(ctx, hp.data(), part.p, hp.size() * sizeof(double));
+  GridSpec gs{};
+  gs.d = d;
+  double span[kGridMaxD];
+  for (int q = 0; q < d; ++q) {
+    double a = INFINITY, b = -INFINITY;
+    for (int t = 0; t < nb; ++t) {
+      const double u = hp[(size_t)t * 2 * d + q];
+      if (std::isnan(u)) return false;  // non-finite coordinates: exact scan keeps numpy's NaN order
+      a = std::min(a, u);
+      b = std::max(b, hp[(size_t)t * 2 * d + d + q]);
+    }
+    gs.lo[q] = a;
+    span[q] = b - a;
+  }
+  // ~2 points per cell over the non-degenerate dimensions
+  int live = 0;
+  for (int q = 0; q < d; ++q) live += span[q] > 0.0;
+  const double per = live ? std::pow((double)n / 2.0, 1.0 / live) : 1.0;
+  int64_t ncells = 1;
+  for (int q = 0; q < d; ++q) {
+    gs.G[q] = span[q] > 0.0 ? std::max<int64_t>(1, (int64_t)per) : 1;
+    gs.h[q] = span[q] > 0.0 ? span[q] / (double)gs.G[q] * (1.0 + 1e-12) : 1.0;
+    ncells *= gs.G[q];
+  }
+  gs.sqmax = max_f64_const(ctx, sq, n);
+  DBuf<int64_t> cell(ctx, n), cell2(ctx, n), id(ctx, n), id2(ctx, n), start(ctx, ncells + 1);
+  k_cells<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, st>>>(n, gs, X, cell.p, id.p);
+  MG_CHECK_LAUNCH(ctx);
+  int bits = 1;
+  while (bits < 63 && ((int64_t)1 << bits) <= ncells) ++bits;
+  size_t tb = 0;
+  MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, cell.p, cell2.p, id.p, id2.p, n, 0, bits, st));
+  DBuf<unsigned char> tmp(ctx, tb);
+  MG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, cell.p, cell2.p, id.p, id2.p, n, 0, bits, st));
+  ctx->launches++;
+  k_cell_starts<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, st>>>(n, ncells, cell2.p, start.p);
+  MG_CHECK_LAUNCH(ctx);
+  DBuf<double> Xs(ctx, (size_t)n * d), sqs(ctx, n);
+  k_gather_sorted<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, st>>>(n, d, id2.p, X, sq, Xs.p,
+                                                                      sqs.p);
+  MG_CHECK_LAUNCH(ctx);
+  const unsigned g = (unsigned)((n + 127) / 128);
+  if (d == 1)
+    k_knn_grid<1><<<g, 128, 0, st>>>(n, k, gs, id2.p, Xs.p, sqs.p, start.p, nbr);
+  else if (d == 2)
+    k_knn_grid<2><<<g, 128, 0, st>>>(n, k, gs, id2.p, Xs.p, sqs.p, start.p, nbr);
+  else
+    k_knn_grid<3><<<g, 128, 0, st>>>(n, k, gs, id2.p, Xs.p, sqs.p, start.p, nbr);
+  MG_CHECK_LAUNCH(ctx);
+  sync(ctx);
+  return true;
+}
+
 __global__ void k_knn_keys(int64_t n, int k, const int64_t *__restrict__ nbr,
                            int64_t *__restrict__ key) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * k;
@@ -118,36 +367,6 @@ __global__ void k_knn_edge_d2(int64_t E, int64_t n, int d, const double *__restr
     const int64_t i = key[e] / n, j = key[e] % n;
     d2[e] = pair_d2(X + i * d, X + j * d, d, sq[i], sq[j]);
   }
-}
-
-// numpy's pairwise summation (DOUBLE_pairwise_sum, PW_BLOCKSIZE 128) on one
-// thread, so sigma2 is the reference's bit for bit
-__device__ double np_pairwise_leaf(const double *a, int64_t n) {
-  if (n < 8) {
-    double r = 0.0;  // numpy: res = 0.; res += a[i] (the -0.0 corner aside)
-    for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
-    return r;
-  }
-  double r[8];
-  for (int q = 0; q < 8; ++q) r[q] = a[q];
-  int64_t i = 8;
-  for (; i < n - (n % 8); i += 8)
-    for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], a[i + q]);
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-  return res;
-}
-
-__device__ double np_pairwise(const double *a, int64_t n) {
-  if (n <= 128) return np_pairwise_leaf(a, n);
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(np_pairwise(a, n2), np_pairwise(a + n2, n - n2));
-}
-
-__global__ void k_np_pairwise_sum(const double *__restrict__ a, int64_t n, double *__restrict__ out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) *out = np_pairwise(a, n);
 }
 
 // both half-edges of every pair: key (row * n + col), weight
@@ -198,9 +417,11 @@ KnnResult knn_graph(mg_ctx *ctx, int64_t n, int d, const double *X, int k, bool 
   MG_CHECK_LAUNCH(ctx);
   const int64_t nk = n * k;
   DBuf<int64_t> nbr(ctx, nk), key(ctx, nk), key2(ctx, nk), ne(ctx, 1);
-  k_knn_topk<<<(unsigned)((n + kKnnThreads - 1) / kKnnThreads), kKnnThreads, 0, st>>>(n, d, k, X,
-                                                                                   sq.p, nbr.p);
-  MG_CHECK_LAUNCH(ctx);
+  if (!knn_topk_grid(ctx, n, d, X, sq.p, k, nbr.p)) {
+    k_knn_topk<<<(unsigned)((n + kKnnThreads - 1) / kKnnThreads), kKnnThreads, 0, st>>>(
+        n, d, k, X, sq.p, nbr.p);
+    MG_CHECK_LAUNCH(ctx);
+  }
   k_knn_keys<<<grid_for(nk, 256, ctx->num_sms * 8), 256, 0, st>>>(n, k, nbr.p, key.p);
   MG_CHECK_LAUNCH(ctx);
   size_t tb1 = 0, tb2 = 0;
@@ -211,16 +432,12 @@ KnnResult knn_graph(mg_ctx *ctx, int64_t n, int d, const double *X, int k, bool 
   MG_CUDA(cub::DeviceSelect::Unique(tmp.p, tb2, key2.p, key.p, ne.p, nk, st));
   int64_t E = 0;
   d2h_sync(ctx, &E, ne.p, sizeof(int64_t));
-  DBuf<double> d2(ctx, E > 0 ? E : 1), s(ctx, 1);
+  DBuf<double> d2(ctx, E > 0 ? E : 1);
   k_knn_edge_d2<<<grid_for(E, 256, ctx->num_sms * 8), 256, 0, st>>>(E, n, d, X, sq.p, key.p, d2.p);
   MG_CHECK_LAUNCH(ctx);
   double sigma2 = 1.0;
   if (weighted) {
-    k_np_pairwise_sum<<<1, 32, 0, st>>>(d2.p, E, s.p);
-    MG_CHECK_LAUNCH(ctx);
-    double sum;
-    d2h_sync(ctx, &sum, s.p, sizeof(double));
-    sigma2 = sum / (double)E;  // dist2.mean()
+    sigma2 = np_sum_f64(ctx, d2.p, E) / (double)E;  // dist2.mean(), numpy's pairwise sum
   }
   r.sigma2 = sigma2;
   const int64_t m = 2 * E;

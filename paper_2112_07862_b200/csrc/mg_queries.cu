@@ -34,12 +34,51 @@ __device__ double pw_leaf(const double *a, int64_t n) {
   return res;
 }
 
+// numpy's split tree walked without recursion (post-order, explicit stack):
+// leaf(off, len, depth, path) is summed for every node with len <= 128 or
+// depth == max_depth, and sibling sums are added left + right
+template <typename Leaf>
+__device__ double pw_tree(int64_t n, int max_depth, Leaf leaf) {
+  struct Fr {
+    int64_t off, len;
+    int depth;
+    uint32_t path;
+    int state;
+    double left;
+  };
+  Fr st[64];
+  int sp = 0;
+  st[0] = {0, n, 0, 0u, 0, 0.0};
+  double ret = 0.0;
+  while (true) {
+    Fr &f = st[sp];
+    if (f.len <= 128 || f.depth == max_depth) {
+      ret = leaf(f.off, f.len, f.depth, f.path);
+    } else {
+      int64_t n2 = f.len / 2;
+      n2 -= n2 % 8;
+      if (f.state == 0) {
+        f.state = 1;
+        st[sp + 1] = {f.off, n2, f.depth + 1, f.path * 2u, 0, 0.0};
+        ++sp;
+        continue;
+      }
+      if (f.state == 1) {
+        f.left = ret;
+        f.state = 2;
+        st[sp + 1] = {f.off + n2, f.len - n2, f.depth + 1, f.path * 2u + 1u, 0, 0.0};
+        ++sp;
+        continue;
+      }
+      ret = __dadd_rn(f.left, ret);
+    }
+    if (sp == 0) return ret;
+    --sp;
+  }
+}
+
 __device__ double pw_seq(const double *a, int64_t n) {
-  // explicit stack instead of recursion (depth <= 64)
-  if (n <= 128) return pw_leaf(a, n);
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(pw_seq(a, n2), pw_seq(a + n2, n - n2));
+  return pw_tree(n, 64, [a](int64_t off, int64_t len, int, uint32_t) { return pw_leaf(a + off, len); });
 }
 
 // thread t: follow the bits of t (MSB first) for kPwDepth levels
@@ -65,16 +104,13 @@ __global__ void k_pw_subtrees(const double *__restrict__ a, int64_t n, double *_
   out[t] = pw_seq(a + off, len);
 }
 
-__device__ double pw_combine(int64_t len, int d, uint32_t path, const double *sub) {
-  if (len <= 128 || d == kPwDepth) return sub[path << (kPwDepth - d)];
-  int64_t n2 = len / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(pw_combine(n2, d + 1, path * 2, sub),
-                   pw_combine(len - n2, d + 1, path * 2 + 1, sub));
-}
-
 __global__ void k_pw_top(int64_t n, const double *__restrict__ sub, double *__restrict__ out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) *out = n > 0 ? pw_combine(n, 0, 0, sub) : 0.0;
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  *out = n > 0 ? pw_tree(n, kPwDepth,
+                         [sub](int64_t, int64_t, int d, uint32_t path) {
+                           return sub[path << (kPwDepth - d)];
+                         })
+               : 0.0;
 }
 
 __global__ void k_sq(const double *__restrict__ x, double *__restrict__ y, int64_t n) {

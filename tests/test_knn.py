@@ -83,3 +83,33 @@ def test_device_knn_feeds_embed(gk):
     ref = O.embed(g.n, g.indptr, g.indices, g.weights, 2, tol=1e-8, max_iter=300, seed=42,
                   require_convergence=False)
     np.testing.assert_allclose(emb.eigenvalues, ref["eigenvalues"], rtol=1e-8)
+
+
+@pytest.mark.gpu
+def test_device_knn_grid_matches_reference():
+    """n >= 4096, d <= 3: the cell-grid search (mg_knn.cu) against the reference's
+    own graphs, including exact distance ties (lattice) and uneven density."""
+    import paper_2112_07862_b200 as mg
+    gk = np.load(os.path.join(HERE, "golden", "knn_grid.npz"))
+    for name in gk["names"].tolist():
+        k, wt = (int(v) for v in gk[f"{name}_k"])
+        g = mg.knn_graph(gk[f"{name}_x"], k, weighted=bool(wt))
+        np.testing.assert_array_equal(g.indptr, gk[f"{name}_indptr"], err_msg=name)
+        np.testing.assert_array_equal(g.indices, gk[f"{name}_indices"], err_msg=name)
+        np.testing.assert_allclose(g.weights, gk[f"{name}_weights"], rtol=1e-13, atol=0,
+                                   err_msg=name)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,d,k", [(200_000, 3, 8), (120_000, 2, 12), (50_000, 1, 5)])
+def test_device_knn_grid_equals_all_pairs(monkeypatch, n, d, k):
+    """The grid search returns exactly the all-pairs scan's graph (same arrays)."""
+    import paper_2112_07862_b200 as mg
+    x = np.random.default_rng(n + d).uniform(size=(n, d))
+    x[: n // 10] *= 0.01  # a dense corner: uneven cell occupancy
+    g1 = mg.knn_graph(x, k)
+    monkeypatch.setenv("MG_KNN_GRID", "0")
+    g0 = mg.knn_graph(x, k)
+    assert np.array_equal(g1.indptr, g0.indptr)
+    assert np.array_equal(g1.indices, g0.indices)
+    assert np.array_equal(g1.weights, g0.weights)
