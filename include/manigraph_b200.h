@@ -291,6 +291,26 @@ int mg_load_edge_list_count(const char *path, int32_t threads, int64_t *n, int64
                             int64_t *err_line);
 int mg_load_edge_list_fill(int64_t *indptr, int64_t *indices, double *weights);
 
+/* ---------------------------------------- binary I/O ------
+ * The objects of the text formats above (embedding.py:131-166,
+ * graph.py:147-194) as raw little-endian arrays behind a 64-byte header
+ * (layout in csrc/mg_binio.cu), written / read by `threads` threads with
+ * pwrite / pread (0: hardware concurrency, at most 16).  Host pointers;
+ * eigenvalues / b may be NULL.  Loads check the header (MG_ERR_PARSE) and,
+ * for graphs, the canonical CSR of Graph.from_edges (MG_ERR_INPUT). */
+int mg_save_embedding_bin(const char *path, int64_t n, int32_t k, const double *P,
+                          const double *eigenvalues, const double *b, const char *method,
+                          int32_t threads);
+int mg_load_embedding_bin_dims(const char *path, int64_t *n, int32_t *k, int32_t *has_b,
+                               char *method16);
+int mg_load_embedding_bin(const char *path, double *P, double *eigenvalues, double *b,
+                          int32_t threads);
+int mg_save_graph_bin(const char *path, int64_t n, const int64_t *indptr, const int64_t *indices,
+                      const double *weights, int32_t threads);
+int mg_load_graph_bin_dims(const char *path, int64_t *n, int64_t *nnz);
+int mg_load_graph_bin(const char *path, int64_t *indptr, int64_t *indices, double *weights,
+                      int32_t threads);
+
 /* --------------------------------------- kNN graph -------
  * knn_graph (graph.py:281-315): symmetrized k-nearest-neighbour graph of the
  * rows of X (device n x d row-major fp64), ties at the k-th distance to the

@@ -39,9 +39,13 @@ from .clustering import kmeans, normalize_rows  # noqa: F401
 from .knn import knn_graph  # noqa: F401
 from .textio import (  # noqa: F401
     load_edge_list,
+    load_embedding_bin,
     load_embedding_csv,
+    load_graph_bin,
     save_edge_list,
+    save_embedding_bin,
     save_embedding_csv,
+    save_graph_bin,
 )
 from .errors import (  # noqa: F401
     ConvergenceError,

@@ -99,6 +99,12 @@ SIGNATURES = {
     "mg_save_edge_list": [C.c_char_p, i64, vp, vp, vp, i32],
     "mg_load_edge_list_count": [C.c_char_p, i32, P_i64, P_i64, P_i64],
     "mg_load_edge_list_fill": [vp, vp, vp],
+    "mg_save_embedding_bin": [C.c_char_p, i64, i32, vp, vp, vp, C.c_char_p, i32],
+    "mg_load_embedding_bin_dims": [C.c_char_p, P_i64, C.POINTER(i32), C.POINTER(i32), C.c_char_p],
+    "mg_load_embedding_bin": [C.c_char_p, vp, vp, vp, i32],
+    "mg_save_graph_bin": [C.c_char_p, i64, vp, vp, vp, i32],
+    "mg_load_graph_bin_dims": [C.c_char_p, P_i64, P_i64],
+    "mg_load_graph_bin": [C.c_char_p, vp, vp, vp, i32],
     "mg_knn_graph_fill": [vp, i64, i32, vp, i32, i32, vp, vp],
     "mg_normalize_rows": [vp, i64, i32, vp, vp],
     # multi-GPU (row-partitioned solve)

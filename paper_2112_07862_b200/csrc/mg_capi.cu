@@ -856,6 +856,62 @@ int mg_load_edge_list_fill(int64_t *indptr, int64_t *indices, double *weights) {
   MG_API_END
 }
 
+int mg_save_embedding_bin(const char *path, int64_t n, int32_t k, const double *P,
+                          const double *eigenvalues, const double *b, const char *method,
+                          int32_t threads) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(path != nullptr && (P != nullptr || n * (int64_t)k == 0), MG_ERR_INPUT, "NULL argument");
+  save_embedding_bin(path, n, k, P, eigenvalues, b, method, threads);
+  MG_API_END
+}
+
+int mg_load_embedding_bin_dims(const char *path, int64_t *n, int32_t *k, int32_t *has_b,
+                               char *method16) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(path != nullptr && n != nullptr && k != nullptr && has_b != nullptr, MG_ERR_INPUT,
+          "NULL argument");
+  int64_t kk = 0;
+  int hb = 0;
+  load_embedding_bin(path, n, &kk, &hb, method16, nullptr, nullptr, nullptr, 1);
+  *k = (int32_t)kk;
+  *has_b = hb;
+  MG_API_END
+}
+
+int mg_load_embedding_bin(const char *path, double *P, double *eigenvalues, double *b,
+                          int32_t threads) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(path != nullptr && P != nullptr, MG_ERR_INPUT, "NULL argument");
+  int64_t n = 0, k = 0;
+  int hb = 0;
+  load_embedding_bin(path, &n, &k, &hb, nullptr, P, eigenvalues, b, threads);
+  MG_API_END
+}
+
+int mg_save_graph_bin(const char *path, int64_t n, const int64_t *indptr, const int64_t *indices,
+                      const double *weights, int32_t threads) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(path != nullptr && indptr != nullptr, MG_ERR_INPUT, "NULL argument");
+  save_graph_bin(path, n, indptr, indices, weights, threads);
+  MG_API_END
+}
+
+int mg_load_graph_bin_dims(const char *path, int64_t *n, int64_t *nnz) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(path != nullptr && n != nullptr && nnz != nullptr, MG_ERR_INPUT, "NULL argument");
+  load_graph_bin(path, n, nnz, nullptr, nullptr, nullptr, 1);
+  MG_API_END
+}
+
+int mg_load_graph_bin(const char *path, int64_t *indptr, int64_t *indices, double *weights,
+                      int32_t threads) {
+  MG_API_BEGIN((mg_ctx *)nullptr)
+  require(path != nullptr && indptr != nullptr, MG_ERR_INPUT, "NULL argument");
+  int64_t n = 0, nnz = 0;
+  load_graph_bin(path, &n, &nnz, indptr, indices, weights, threads);
+  MG_API_END
+}
+
 int mg_knn_graph_count(mg_ctx *ctx, int64_t n, int32_t d, const double *X, int32_t k,
                        int32_t weighted, int64_t *indptr, int64_t *nnz) {
   MG_API_BEGIN(ctx)
