@@ -1806,6 +1806,14 @@ struct Lobpcg {
             break;
           }
         c0 = c0 / VN * VN;
+        {
+          static const bool dbg_c0 = env_double("MG_DEBUG_C0", 0) != 0;
+          if (dbg_c0) {
+            int na = 0;
+            for (int c = 0; c < m; ++c) na += cv[c] ? 0 : 1;
+            fprintf(stderr, "[c0] it=%d c0=%d m=%d active=%d\n", it, c0, m, na);
+          }
+        }
         if (comm)
           halo_spmm(Wc.p, mp, c0, mp - c0, AS.p + 2 * mp + c0, ld);
         else
