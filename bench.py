@@ -424,6 +424,30 @@ def main():
     spmm_ms = sp["ms"] / max(sp["launches"], 1)
     spmm_bytes = sp["bytes"] / max(sp["launches"], 1)
     achieved = spmm_bytes / (spmm_ms / 1e3) / 1e9 if sp["launches"] else 0.0
+    # per-kernel rooflines of the three hot kernels (C5: fp32, m = K + 1, mp = m
+    # padded to 4, w = 3 mp).  SpMM: HBM (SURVEY 8(d) bytes); update: FP32 FMA
+    # pipe (2 * (w*mp + mp*mp) * 2 flop per row, measured 72.56 TFLOP/s,
+    # profiles/r2_fp32_peak.json) and HBM (10 m s_v N); Gram: tensor pipe
+    # (3xTF32 products over the 128 x 128 padded tile, 2 Grams; TF32 dense peak
+    # = bf16 / 2) and HBM (6 m s_v N)
+    m_blk = K + 1
+    mp_blk = (m_blk + 3) // 4 * 4
+    w_blk = 3 * mp_blk
+    rl = {}
+    for kname in ("update", "gram"):
+        if kname in st and st[kname]["launches"]:
+            avg_s = st[kname]["ms"] / st[kname]["launches"] / 1e3
+            if kname == "update":
+                flops = 2.0 * (w_blk * mp_blk + mp_blk * mp_blk) * 2 * n
+                rl["update"] = {"bound": "fp32-fma", "achieved": flops / avg_s / 1e12,
+                                "peak": 72.56, "unit": "TFLOP/s",
+                                "frac": flops / avg_s / 1e12 / 72.56,
+                                "hbm_frac": 10 * m_blk * 4 * n / avg_s / 1e9 / hbm}
+            else:
+                flops = 2.0 * 2 * 3 * 128 * 128 * n
+                rl["gram"] = {"bound": "tensor", "achieved": flops / avg_s / 1e12,
+                              "peak": bf16 / 2, "unit": "TFLOP/s", "frac": flops / avg_s / 1e12 / (bf16 / 2),
+                              "hbm_frac": 6 * m_blk * 4 * n / avg_s / 1e9 / hbm}
     kern = {k: {"launches": v["launches"], "ms_per_step": v["ms"] / args.steps,
                 "avg_us": 1e3 * v["ms"] / max(v["launches"], 1),
                 "GB_per_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
@@ -446,6 +470,7 @@ def main():
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": spmm_bytes, "avg_launch_ms": spmm_ms},
         "kernels": kern,
+        "rooflines_other": rl,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "note": "mg.embed(Graph(host arrays)): H2D graph, device PCG64/ziggurat normal stream, D2H P and b"},
         "gpu_launches": int(launches / max(args.steps, 1)),
