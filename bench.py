@@ -434,7 +434,10 @@ def main():
     mp_blk = (m_blk + 3) // 4 * 4
     w_blk = 3 * mp_blk
     rl = {}
-    for kname in ("update", "gram"):
+    tc_gram = prec == "fp32" and 48 < w_blk <= 128  # k_gram_tc2 (else the CUDA-core k_gram2)
+    for kname in ("update", "gram") if prec == "fp32" else ():
+        if kname == "gram" and not tc_gram:
+            continue
         if kname in st and st[kname]["launches"]:
             avg_s = st[kname]["ms"] / st[kname]["launches"] / 1e3
             if kname == "update":
