@@ -255,7 +255,18 @@ void spmm(mg_ctx *ctx, const DevCSR<T> &A, const T *X, int ldx, T *Y, int ldy, i
   require(L >= 1 && L <= 32 && w % VN == 0, MG_ERR_INTERNAL, "spmm width");
   int G = 32 / L;
   int64_t rows_per_block = 8 * G;
-  int grid = grid_for(A.n, (int)rows_per_block, ctx->num_sms * 64);
+  // grid-stride sweep with up to 256 CTAs per SM: the active rows are spread
+  // over ~n / (resident CTAs x 24) windows of the matrix.  Measured at C5 20M
+  // (ms per narrow launch): a coherent sweep with only the resident CTAs 12.1,
+  // one 24-row chunk per CTA 9.8, caps of 16 / 32 / 64 / 128 / 256 / 512 x SMs
+  // 11.1 / 9.96 / 9.41 / 9.23 / 9.13 / 9.10 -- spreading the gathers over more
+  // of the matrix beats keeping them coherent; the L2 policy of the gathered
+  // rows (evict_last vs normal) made no difference (9.15 / 9.12).
+  static const int grid_cap = [] {
+    const char *e = getenv("MG_SPMM_GRID");
+    return e ? std::max(1, atoi(e)) : 256;
+  }();
+  int grid = grid_for(A.n, (int)rows_per_block, ctx->num_sms * grid_cap);
   // algorithmic bytes: values+indices, row pointers, X read once, Y written once
   double bytes = (double)A.nnz * (sizeof(T) + sizeof(int)) + 8.0 * (A.n + 1) +
                  2.0 * sizeof(T) * (double)A.n * w;
