@@ -2,7 +2,7 @@
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden_scale.py NAME [NAME ...]
 
-NAME is one of ``c3_1M c4_500K c5_1M c5_2M c5_200K hub``.  Runs the
+NAME is one of ``c3_1M c3_100K c4_500K c5_1M c5_2M c5_200K hub defl2 queries``.  Runs the
 UNMODIFIED reference (``manigraph`` from /root/reference/pkg/src, build
 container only) on the harness graphs of ``paper_2112_07862_b200.synthetic``
 and writes ``scale_<NAME>.json`` (+ ``scale_<NAME>.npz`` for small arrays):
@@ -15,7 +15,7 @@ and writes ``scale_<NAME>.json`` (+ ``scale_<NAME>.npz`` for small arrays):
   (operators.py:189-219) at 8192 fixed sampled rows plus its sum / sum of
   squares / dot with a fixed random vector (b is reproduced to ~1e-15, not
   bit for bit, so a hash would not do);
-* for ``c5_200K``: tight generalized eigenpairs of the reference's (A, B)
+* for ``c5_200K`` and ``c3_100K``: tight generalized eigenpairs of the reference's (A, B)
   (scipy eigsh shift-invert, tol 1e-12; vectors stored as float32, the
   sign convention of eigensolver.py:83-89) and the reference's own
   ``lobpcg_smallest`` at the config tolerance (eigenvalues, iterations, and
@@ -58,6 +58,7 @@ CASES = {
     "c5_1M": ("c5", 1_000_000, False),
     "c5_2M": ("c5", 2_000_000, False),
     "c5_200K": ("c5", 200_000, True),
+    "c3_100K": ("c3", 100_000, True),
 }
 B_SAMPLE = 8192
 
