@@ -83,7 +83,9 @@ def test_c2_fp64_eigenpairs(mg, golden_c2, c2_graph, reorder):
     # B-orthonormality of the returned block
     gram = vecs.T @ (b[:, None] * vecs)
     assert np.max(np.abs(gram - np.eye(5))) < 1e-8
-    assert abs(res.iterations - meta["solve"]["iterations"]) <= 60
+    # the reference needs 1001; measured 1001 (reordered) and 998 (natural
+    # order): the last pair crosses tol 1e-6 inside the F5 noise band
+    assert abs(res.iterations - meta["solve"]["iterations"]) <= 5, res.iterations
 
 
 def _angles_vs_tight(z, vecs, b):
