@@ -12,7 +12,8 @@ what the reference computed:
   1e-10 relative in fp64 (SURVEY 8(c) protocol item 2);
 * mu: exact;  b: 1e-13 relative at 8192 sampled rows plus global sums;
 * ``OperatorPair.diagnostics()`` keys equal;
-* C5 family at 200K (K = 32, fp32, tol 1e-4): eigenvalues within the
+* C5 family at 200K (K = 32, fp32, tol 1e-4) and C3 family at 100K (K = 8,
+  tol 1e-5): eigenvalues within the
   north_star's 1e-4 relative of the reference's own LOBPCG and of the tight
   (shift-invert) eigenvalues; complete-cluster principal angles within
   max(1e-3, 2.5 x the reference's own angle) of the tight vectors, plus the
@@ -33,7 +34,7 @@ from conftest import GOLDEN, principal_angles
 
 pytestmark = pytest.mark.gpu
 
-CASES = ["c5_200K", "c3_1M", "c4_500K", "c5_1M", "c5_2M"]
+CASES = ["c5_200K", "c3_100K", "c3_1M", "c4_500K", "c5_1M", "c5_2M"]
 
 
 def sha(a):
@@ -113,24 +114,30 @@ def test_operator_pair_matches_reference(mg, name):
     assert d["min_disc_left_end"] == pytest.approx(rd["min_disc_left_end"], rel=1e-12, abs=1e-300)
 
 
-def test_c5_200k_eigenpairs_vs_reference(mg):
-    z, meta = load("c5_200K")
+@pytest.mark.parametrize("name", ["c5_200K", "c3_100K"])
+def test_eigenpairs_vs_reference(mg, name):
+    """C5 family (cube, K = 32, tol 1e-4) at 200K and C3 family (sphere, K = 8,
+    tol 1e-5) at 100K, fp32 with fp64 Gram, against the reference's own LOBPCG
+    and the tight shift-invert solution of the reference's (A, B)."""
+    z, meta = load(name)
     if "tight" not in meta or "clusters" not in meta:
         pytest.skip("tight solution not in the golden")
-    from paper_2112_07862_b200 import core
-    g = graph("c5_200K", meta)
-    cfg = mg.SolverConfig(k=33, tol=1e-4, max_iter=3000, seed=42, precision="fp32")
-    res, bt, dg = core.embed_arrays(*g, 32, cfg)
+    from paper_2112_07862_b200 import core, synthetic
+    c = synthetic.CONFIGS[meta["config"]]
+    g = graph(name, meta)
+    m = c.k + 1
+    cfg = mg.SolverConfig(k=m, tol=c.tol, max_iter=3000, seed=42, precision="fp32")
+    res, bt, dg = core.embed_arrays(*g, c.k, cfg)
     assert res.converged.all()
     ev = res.eigenvalues
     vecs = res.eigenvectors.cpu().numpy()
     b = bt.cpu().numpy()
-    tight = z["tight_eigenvalues"][:33]
+    tight = z["tight_eigenvalues"][:m]
     ref = z["ref_eigenvalues"]
     # north_star: fp32 eigenvalues within 1e-4 relative of the oracle, on the
-    # complete eigenvalue clusters (the cluster cut by the block edge, columns
-    # 29-32, is resolved only to the solver tolerance by either side: the
-    # reference's own columns there are 0.013-0.042 rad from the tight vectors)
+    # complete eigenvalue clusters (a cluster cut by the block edge -- C5
+    # columns 29-32 -- is resolved only to the solver tolerance by either side:
+    # the reference's own columns there are 0.013-0.042 rad from the tight vectors)
     comp = sorted(j for c in meta["clusters"]["complete"] for j in c)
     rel_ref = np.abs(ev - ref) / ref
     assert np.max(rel_ref[comp]) < 1e-4, rel_ref
