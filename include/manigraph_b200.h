@@ -257,6 +257,21 @@ int mg_embed_host(mg_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *
 int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float *S,
                      const float *AS, const float *b, double *GB, double *GA);
 
+/* One LOBPCG basis update of the fp32 solve, in place on row-major n x ld
+ * fp32 blocks S = [X | P | W] and AS = [AX | AP | AW] (column blocks of width
+ * mp, m <= mp real columns), eigensolver.py:255-266:
+ *   P = S Zp, X = X Yx + P, AP = AS Zp, AX = AX Yx + AP,
+ *   R = AX - b X Theta (eigensolver.py:225), W = prec R (eigensolver.py:239),
+ * M = [Zp (3mp x mp) ; Yx (mp x mp)] row-major fp32, theta fp64 (m), prec may
+ * be NULL.  W is also written to the compact n x mp block wc (the SpMM input).
+ * colsums (2 mp, fp64): sum R^2 per column, then sum X^2 per column.
+ * variant 0: fp32 FMA kernel; variant 1: tcgen05 (3 mp <= 128), which forms
+ * only the corrections X (Yx - I) + P on the tensor core and adds them to the
+ * old X / AX in fp32. */
+int mg_update_f32(mg_ctx *ctx, int32_t variant, int64_t n, int32_t ld, int32_t m, int32_t mp,
+                  float *S, float *AS, const float *b, const float *prec, const float *M,
+                  const double *theta, float *wc, double *colsums);
+
 /* Host <-> device copies for large pageable host buffers (results, inputs):
  * pipelined through the context's pinned stages; blocking. */
 int mg_copy_d2h(mg_ctx *ctx, void *host, const void *dev, int64_t bytes);

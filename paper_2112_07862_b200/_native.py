@@ -88,6 +88,7 @@ SIGNATURES = {
     "mg_embed_host": [vp, i64, vp, vp, vp, i32, C.POINTER(SolverCfg), i32, i32, i32, vp, i64,
                       vp, vp, C.POINTER(SolverOut), C.POINTER(EmbedDiag)],
     "mg_gram_pair_f32": [vp, i64, i32, i32, vp, vp, vp, vp, vp],
+    "mg_update_f32": [vp, i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp],
     "mg_kmeans": [vp, i64, i32, vp, i32, i32, C.c_uint64, vp, P_f64],
     "mg_knn_graph_count": [vp, i64, i32, vp, i32, i32, vp, P_i64],
     "mg_normal_stream": [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, i64, vp],

@@ -769,6 +769,19 @@ int mg_gram_pair_f32(mg_ctx *ctx, int64_t n, int32_t ld, int32_t w, const float 
   MG_API_END
 }
 
+int mg_update_f32(mg_ctx *ctx, int32_t variant, int64_t n, int32_t ld, int32_t m, int32_t mp,
+                  float *S, float *AS, const float *b, const float *prec, const float *M,
+                  const double *theta, float *wc, double *colsums) {
+  MG_API_BEGIN(ctx)
+  require(n >= 1 && m >= 1 && mp >= m && mp % 4 == 0 && ld >= 3 * mp && ld % 4 == 0, MG_ERR_INPUT,
+          "bad update shape");
+  require(variant == 0 || update_tc3_supported(3 * mp, mp, ld), MG_ERR_INPUT,
+          "tensor-core update needs 3 mp <= 128");
+  update_f32_hook(ctx, variant, n, ld, m, mp, S, AS, b, prec, M, theta, wc, colsums);
+  sync(ctx);
+  MG_API_END
+}
+
 int mg_copy_d2h(mg_ctx *ctx, void *host, const void *dev, int64_t bytes) {
   MG_API_BEGIN(ctx)
   require(bytes >= 0 && (bytes == 0 || (host && dev)), MG_ERR_INPUT, "bad copy arguments");

@@ -33,6 +33,27 @@
 
 namespace mg {
 
+// debug (MG_UPD_TC_CHECK): per column block of width mp, max |a - b| and max |b|
+__global__ void k_upd_cmp(const float *__restrict__ a, const float *__restrict__ b, int64_t n,
+                          int ld, int mp, int nblk, float *out) {
+  float d[4] = {0, 0, 0, 0}, v[4] = {0, 0, 0, 0};
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * ld;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int col = (int)(e % ld), blk = col / mp;
+    if (blk < nblk) {
+      const float x = a[e], y = b[e];
+      const float df = (x == y) ? 0.f : fabsf(x - y);  // NaN -> NaN propagates below
+      d[blk] = (df > d[blk] || df != df) ? (df != df ? 3.0e38f : df) : d[blk];
+      v[blk] = fmaxf(v[blk], fabsf(y));
+    }
+  }
+  for (int q = 0; q < nblk; ++q) {
+    atomicMax(reinterpret_cast<int *>(out + 2 * q), __float_as_int(d[q]));
+    atomicMax(reinterpret_cast<int *>(out + 2 * q + 1), __float_as_int(v[q]));
+  }
+}
+
+
 static constexpr int kTR = 32;           // rows per tile pass tile
 static constexpr int kPassThreads = 256;
 static constexpr int kGT = 3;            // Gram register tiles per thread
@@ -1609,12 +1630,63 @@ struct Lobpcg {
     ua.skip = status.p + 5;
     ua.wc = Wc.p;
     ua.part = colpart.p;
+    ua.emul = (int)env_double("MG_UPD_EMUL", 0);
     int nblk_upd = grid_upd;
     {
       ProfScope ps(ctx, PROF_UPDATE, 2.0 * n * ld * sizeof(T) + 5.0 * n * mp * sizeof(T));
       const T *pr = sp.jacobi ? prec.p : nullptr;
       if constexpr (sizeof(T) == 4) {
-        if (upd_ws) {
+        static const int upd_tc = (int)env_double("MG_UPD_TC", 0);
+        static const int upd_tc_check = (int)env_double("MG_UPD_TC_CHECK", 0);
+        if (upd_tc && upd_tc_check && upd_ws && update_tc3_supported(w, mp, ld) &&
+            (iter_now % upd_tc_check) == (upd_tc_check > 1 ? 1 : 0)) {
+          // debug: the CUDA-core update on copies, compared block by block below
+          DBuf<float> S2(ctx, (size_t)n * ld), A2(ctx, (size_t)n * ld), W2(ctx, (size_t)n * mp);
+          DBuf<double> cp2(ctx, (size_t)ctx->num_sms * 4 * 2 * mp);
+          DBuf<float> out(ctx, 32);
+          out.zero();
+          MG_CUDA(cudaMemcpyAsync(S2.p, S.p, (size_t)n * ld * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+          MG_CUDA(cudaMemcpyAsync(A2.p, AS.p, (size_t)n * ld * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+          UpdArgs uw = ua;
+          uw.tk = tk_ws;
+          uw.wc = W2.p;
+          uw.part = cp2.p;
+          k_update_ws<4><<<grid_upd, kWsF + kWsS, ws_smem, ctx->stream>>>(
+              S2.p, A2.p, (const float *)bw.p, (const float *)pr, (const float *)M.p, theta.p, uw);
+          MG_CHECK_LAUNCH(ctx);
+          nblk_upd = update_tc3(ctx, n, ld, w, m, mp, (float *)S.p, (float *)AS.p,
+                                (const float *)bw.p, (const float *)pr, (const float *)M.p,
+                                theta.p, status.p + 5, colpart.p, (float *)Wc.p);
+          k_upd_cmp<<<4 * ctx->num_sms, 256, 0, ctx->stream>>>((const float *)S.p, S2.p, n, ld, mp, 3, out.p);
+          k_upd_cmp<<<4 * ctx->num_sms, 256, 0, ctx->stream>>>((const float *)AS.p, A2.p, n, ld, mp, 2, out.p + 8);
+          k_upd_cmp<<<4 * ctx->num_sms, 256, 0, ctx->stream>>>((const float *)Wc.p, W2.p, n, mp, mp, 1, out.p + 16);
+          float h[32];
+          d2h_sync(ctx, h, out.p, sizeof(h));
+          std::vector<double> c1((size_t)2 * mp), c2((size_t)2 * mp);
+          k_reduce_cols<<<reduce_cols_grid(2 * mp), 256, 0, ctx->stream>>>(colpart.p, nblk_upd, 2 * mp, colred.p);
+          d2h_sync(ctx, c1.data(), colred.p, c1.size() * 8);
+          k_reduce_cols<<<reduce_cols_grid(2 * mp), 256, 0, ctx->stream>>>(cp2.p, grid_upd, 2 * mp, colred.p);
+          d2h_sync(ctx, c2.data(), colred.p, c2.size() * 8);
+          double nd = 0;
+          for (size_t e = 0; e < c1.size(); ++e)
+            nd = std::max(nd, std::abs(c1[e] - c2[e]) / (std::abs(c2[e]) + 1e-300));
+          bool bad = nd > 1e-3;
+          for (int q : {0, 2, 4, 8, 10, 16}) bad = bad || !(h[q] <= 3e-5f * h[q + 1]);
+          if (bad || (iter_now % 40) == 1)
+          fprintf(stderr,
+                  "[upd_tc it=%d] maxdiff/maxabs X %.2e/%.2e P %.2e/%.2e W %.2e/%.2e | AX %.2e/%.2e "
+                  "AP %.2e/%.2e | Wc %.2e/%.2e | norms rel %.2e\n",
+                  iter_now, h[0], h[1], h[2], h[3], h[4], h[5], h[8], h[9], h[10], h[11], h[16], h[17],
+                  nd);
+          goto upd_done;
+        }
+        if (upd_tc && !ua.emul && update_tc3_supported(w, mp, ld) && w > upd_tc) {
+          nblk_upd = update_tc3(ctx, n, ld, w, m, mp, (float *)S.p, (float *)AS.p,
+                                (const float *)bw.p, (const float *)pr, (const float *)M.p,
+                                theta.p, status.p + 5, colpart.p, (float *)Wc.p);
+          goto upd_done;
+        }
+        if (upd_ws && !ua.emul) {
           UpdArgs uw = ua;
           uw.tk = tk_ws;
           k_update_ws<4><<<grid_upd, kWsF + kWsS, ws_smem, ctx->stream>>>(

@@ -22,4 +22,14 @@ bool gram_tc2_supported(int w, int ld);
 void gram_pair_tc2(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const float *AS,
                    const float *b, double *GB, double *GA, DBuf<double> &part);
 
+// tcgen05 update (mg_tc3.cu): P = S Zp, X += S (Zp + [Yx - I; 0; 0]) and the
+// A-images, fused residual / W / column norms; returns the grid (rows of part)
+bool update_tc3_supported(int w, int mp, int ld);
+int update_tc3(mg_ctx *ctx, int64_t n, int ld, int w, int m, int mp, float *S, float *AS,
+               const float *b, const float *prec, const float *Mg, const double *theta,
+               const int *skip, double *part, float *wc);
+void update_f32_hook(mg_ctx *ctx, int variant, int64_t n, int ld, int m, int mp, float *S,
+                     float *AS, const float *b, const float *prec, const float *Mg,
+                     const double *theta, float *wc, double *colsums);
+
 }  // namespace mg
