@@ -1842,7 +1842,11 @@ struct Lobpcg {
         double qn = std::sqrt(cr[mp + c]);
         cv[c] = rn[c] <= tol * ((anorm + std::fabs(th[c]) * bmax) * qn) ? 1 : 0;
       }
-      return std::all_of(cv.begin(), cv.end(), [](int v) { return v != 0; });
+      // experiment (MG_CONV_COLS): only the first columns have to converge; the
+      // rest of the block rides along as guard vectors
+      static const int conv_cols = (int)env_double("MG_CONV_COLS", 0);
+      const int need = sizeof(T) == 4 && conv_cols > 0 && conv_cols < m ? conv_cols : m;
+      return std::all_of(cv.begin(), cv.begin() + need, [](int v) { return v != 0; });
     };
     std::vector<double> rn;
     std::vector<int> cv;

@@ -53,12 +53,12 @@ constexpr int kU3Acc = 128;            // TMEM column of the accumulators (Z2' s
 __host__ __device__ constexpr size_t u3_xbytes(int mp) {
   return ((size_t)2 * kU3Rows * mp * 4 + 127) / 128 * 128;  // old X and AX columns of a tile
 }
-// output staging per (row half, slot): 16 complete rows of [X P W] (3mp),
-// [AX AP] (2mp) and compact W (mp)
+// output staging per row group: 16 complete rows of [X P W] (3mp), [AX AP]
+// (2mp) and compact W (mp)
 __host__ __device__ constexpr size_t u3_obytes(int mp) { return (size_t)16 * 6 * mp * 4; }
 __host__ __device__ constexpr size_t u3_smem(int np, int mp) {
   return (size_t)kU3NR * np * kU3Box + (size_t)kU3NL * kU3Box + u3_xbytes(mp) +
-         4 * u3_obytes(mp) + 512;
+         3 * u3_obytes(mp) + 512;
 }
 
 // K-major SWIZZLE_128B operand (8-row x 128-byte atoms, SBO = 1024)
@@ -176,14 +176,16 @@ __device__ __forceinline__ void mbar_wait_bk(uint64_t *bar, uint32_t phase) {
 
 // Warp roles (16 warps; warp w runs on scheduler w % 4, and only warps with
 // w % 4 == q can read TMEM lanes 32q .. 32q + 31):
-//   epilogue  4, 8 (q = 0)   5, 9 (q = 1)   6, 10 (q = 2)      [lane = output column]
-//   splitters 2, 14, 7, 11   TMA producer 3   MMA issuer 15   (0, 1, 12, 13 idle)
-// so the heavy X-column quadrants share their schedulers with idle warps only.
+//   epilogue  0, 4, 8 (q = 0)   1, 5, 9 (q = 1)   2, 6, 10 (q = 2)   [lane = output column;
+//             three row groups of 32 rows: the per-chunk dependency chain, not the
+//             instruction count, bounds a warp, so more warps in flight pay]
+//   splitters 13, 14, 7, 11   TMA producers 3 (tiles), 12 (old X / AX)   MMA issuer 15
 template <int MP>
 __global__ void __launch_bounds__(kU3Threads, 1)
     k_update_tc3(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmA,
                  const __grid_constant__ CUtensorMap tmXS, const __grid_constant__ CUtensorMap tmXA,
-                 float *S, float *AS, const float *__restrict__ b,
+                 const __grid_constant__ CUtensorMap tmOS, const __grid_constant__ CUtensorMap tmOA,
+                 const __grid_constant__ CUtensorMap tmOW, float *S, float *AS, const float *__restrict__ b,
                  const float *__restrict__ prec, const float *__restrict__ Mg,
                  const double *__restrict__ theta, Upd3Args a) {
   if (*a.skip) return;
@@ -195,12 +197,13 @@ __global__ void __launch_bounds__(kU3Threads, 1)
   unsigned char *los = raw + (size_t)kU3NR * MT;
   float *xbuf = reinterpret_cast<float *>(los + (size_t)kU3NL * kU3Box);  // [2][rows][MP]
   float *obuf = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(xbuf) +
-                                          u3_xbytes(MP));  // [row half][2 slots]
+                                          u3_xbytes(MP));  // [row group]
   uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(obuf) +
-                                                4 * u3_obytes(MP));
+                                                3 * u3_obytes(MP));
   uint64_t *full = bars, *rempty = full + kU3NR, *lfull = rempty + kU3NR, *lempty = lfull + kU3NL;
-  constexpr int NC = kU3Rows / 32;  // 16-row chunks per tile and row half
-  constexpr int NX = 2 * NC;        // X staging slots: one per (row half, chunk)
+  constexpr int NG = 3;                   // epilogue row groups (32 rows of a tile each)
+  constexpr int NC = kU3Rows / (16 * NG);  // 16-row chunks per tile and row group
+  constexpr int NX = NG * NC;              // X staging slots: one per (row group, chunk)
   uint64_t *afull = lempty + kU3NL, *aempty = afull + 2, *xfull = aempty + 2, *xempty = xfull + NX;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(xempty + NX);
 
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(kU3Threads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&afull[s], 1);
-      mbar_init(&aempty[s], 2 * NQ);
+      mbar_init(&aempty[s], NG * NQ);
     }
     for (int s = 0; s < NX; ++s) {
       mbar_init(&xfull[s], 1);
@@ -337,9 +340,9 @@ __global__ void __launch_bounds__(kU3Threads, 1)
       // tile as soon as its NQ reader warps have taken their values
       for (int ti = 0; ti < T; ++ti)
         for (int ch = 0; ch < NC; ++ch)
-          for (int hf = 0; hf < 2; ++hf) {
+          for (int hf = 0; hf < NG; ++hf) {
             const int sl = hf * NC + ch;
-            const int r0 = (int)((t_begin + ti) * kU3Rows) + hf * (kU3Rows / 2) + ch * 16;
+            const int r0 = (int)((t_begin + ti) * kU3Rows) + hf * (kU3Rows / NG) + ch * 16;
             float *dst = xbuf + sl * (2 * 16 * MP);
             mbar_wait_bk(&xempty[sl], (ti & 1) ^ 1);
             mbar_expect_tx(&xfull[sl], 2 * 16 * MP * 4);
@@ -348,12 +351,12 @@ __global__ void __launch_bounds__(kU3Threads, 1)
           }
     }
     __syncwarp();
-  } else if (warp == 2 || warp == 14 || warp == 7 || warp == 11) {
+  } else if (warp == 13 || warp == 14 || warp == 7 || warp == 11) {
     // ------------------------------------------------------------ splitters
     // hi = rn_tf32(x) in place, lo = rn_tf32(x - hi); 16-byte chunks whose
     // columns lie beyond the last k-step are skipped (128-byte rows, chunk
     // XOR-swizzled with the row)
-    const int st = (warp == 2 ? 0 : warp == 14 ? 1 : warp == 7 ? 2 : 3) * 32 + lane;  // 0..127
+    const int st = (warp == 13 ? 0 : warp == 14 ? 1 : warp == 7 ? 2 : 3) * 32 + lane;  // 0..127
     constexpr int nchunk = kU3Box / 16;  // per box: 6 per thread
     uint32_t g = 0;
     for (int ti = 0; ti < T; ++ti)
@@ -387,13 +390,13 @@ __global__ void __launch_bounds__(kU3Threads, 1)
           if (lane == 0) arrive(&lfull[j]);
         }
       }
-  } else if (warp >= 4 && warp < 12 && q < NQ) {
+  } else if (warp < 12 && q < NQ) {
     // ------------------------------------------------------------- epilogue
     // Chunks of 16 rows, software-pipelined: the old X / AX values and b / prec
     // of chunk u + 1 are loaded before chunk u is drained, so one L2 round
     // trip is hidden behind a chunk of arithmetic and stores.  LD is a
     // compile-time constant: every row address is base + immediate.
-    const int half = (warp - 4) >> 2;
+    const int half = warp >> 2;  // row group
     const int j = 32 * q + lane;           // output column held by this TMEM lane
     const bool isx = j < MP;
     const int c = isx ? j : j - MP;
@@ -403,7 +406,7 @@ __global__ void __launch_bounds__(kU3Threads, 1)
     double sr = 0.0, sx = 0.0;
     const int64_t NU = (int64_t)T * NC;
     auto row_of = [&](int64_t u) {
-      return (t_begin + u / NC) * kU3Rows + half * (kU3Rows / 2) + (int)(u % NC) * 16;
+      return (t_begin + u / NC) * kU3Rows + half * (kU3Rows / NG) + (int)(u % NC) * 16;
     };
     float bn = 0.f, pn = 1.f;  // next chunk's b / prec (lane & 15 holds row rr + (lane & 15))
     auto load_bp = [&](int64_t u) {
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(kU3Threads, 1)
       {
         // old X / AX columns of this chunk, staged by TMA (exact fp32)
         const int sl = half * NC + ch;
-        mbar_wait_bk(&xfull[sl], ti & 1);
+        if (!(a.dbg & 64)) mbar_wait_bk(&xfull[sl], ti & 1);
         const float *xs = xbuf + sl * (2 * 16 * MP) + c;
         if (actx) {
 #pragma unroll
@@ -440,7 +443,7 @@ __global__ void __launch_bounds__(kU3Threads, 1)
       }
       if (on) {
         const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + kU3Acc + buf * (2 * kU3Rows) +
-                            half * (kU3Rows / 2) + ch * 16;
+                            half * (kU3Rows / NG) + ch * 16;
         float dS[16], dA[16];
         if (!(a.dbg & 16)) {
           tmem_ld16(ta, dS);
@@ -451,14 +454,15 @@ __global__ void __launch_bounds__(kU3Threads, 1)
           for (int e = 0; e < 16; ++e) dS[e] = dA[e] = 0.f;
         }
         // Outputs are staged as complete rows in shared memory (lane = column:
-        // conflict-free), then the warps of this row half copy them out with
-        // 16-byte stores that run along the rows -- full sectors and lines, like
-        // the CUDA-core kernel's store warps.  (Per-lane 4-byte stores of single
-        // column blocks bounded the kernel; TMA stores queued behind the tile
-        // loads.)  Double-buffered slots: one barrier per chunk.
-        const int os = (int)(u & 1);
-        float *oS = obuf + (size_t)(half * 2 + os) * (16 * 6 * MP);
+        // conflict-free) and written by TMA: row-contiguous 432 / 288 / 144-byte
+        // segments, ~10 L2 line transactions per row.  Per-warp 128-byte stores
+        // of single column blocks cost ~18 and bounded the kernel (3.6 ms of
+        // 9.4 at C5).  Rows beyond n are clipped by the tensor maps.
+        float *oS = obuf + (size_t)half * (16 * 6 * MP);
         float *oA = oS + 16 * W, *oW = oA + 16 * 2 * MP;
+        if (q == 0 && lane == 0)  // the previous chunk's stores have read the slot
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        asm volatile("bar.sync %0, %1;" ::"r"(2 + half), "n"(32 * NQ) : "memory");
         // b / prec are uniform per row: shuffled before the lanes split into roles
         float br[16], pr[16];
 #pragma unroll
@@ -497,28 +501,15 @@ __global__ void __launch_bounds__(kU3Threads, 1)
             oA[e * 2 * MP + MP + c] = actp ? dA[e] : 0.f;
           }
         }
+        fence_proxy_async();
         asm volatile("bar.sync %0, %1;" ::"r"(2 + half), "n"(32 * NQ) : "memory");
-        {
-          const int t = 32 * q + lane;
-          constexpr int NT = 32 * NQ, S4 = W / 4, A4 = 2 * MP / 4, W4 = MP / 4;
-          const float4 *s4 = reinterpret_cast<const float4 *>(oS);
-          const float4 *a4 = reinterpret_cast<const float4 *>(oA);
-          const float4 *w4 = reinterpret_cast<const float4 *>(oW);
-#pragma unroll
-          for (int i = t; i < 16 * S4; i += NT) {
-            const int row = i / S4, c4 = i - row * S4;
-            if (row < nrow) *reinterpret_cast<float4 *>(S + (rr + row) * LD + 4 * c4) = s4[i];
+        if (q == 0 && lane == 0) {
+          if (nrow > 0) {
+            tma_st2d(&tmOS, 0, (int)rr, oS);
+            tma_st2d(&tmOA, 0, (int)rr, oA);
+            tma_st2d(&tmOW, 0, (int)rr, oW);
           }
-#pragma unroll
-          for (int i = t; i < 16 * A4; i += NT) {
-            const int row = i / A4, c4 = i - row * A4;
-            if (row < nrow) *reinterpret_cast<float4 *>(AS + (rr + row) * LD + 4 * c4) = a4[i];
-          }
-#pragma unroll
-          for (int i = t; i < 16 * W4; i += NT) {
-            const int row = i / W4;
-            if (row < nrow) reinterpret_cast<float4 *>(a.wc + rr * MP)[i] = w4[i];
-          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
       if (ch == NC - 1) {
@@ -527,17 +518,23 @@ __global__ void __launch_bounds__(kU3Threads, 1)
         if (lane == 0) arrive(&aempty[buf]);
       }
     }
-    // column partials: the two row halves of a column meet in shared memory
+    if (q == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // column partials: the row groups of a column meet in shared memory
     // (the raw ring is idle by now: every box was consumed before the last afull)
     double *red = reinterpret_cast<double *>(raw);
     if (isx) {
       red[(half * MP + c) * 2] = sr;
       red[(half * MP + c) * 2 + 1] = sx;
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(64 * NQ) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * NG * NQ) : "memory");
     if (half == 0 && isx) {
-      a.part[(size_t)blockIdx.x * 2 * MP + c] = red[c * 2] + red[(MP + c) * 2];
-      a.part[(size_t)blockIdx.x * 2 * MP + MP + c] = red[c * 2 + 1] + red[(MP + c) * 2 + 1];
+      double t1 = 0.0, t2 = 0.0;
+      for (int g2 = 0; g2 < NG; ++g2) {
+        t1 += red[(g2 * MP + c) * 2];
+        t2 += red[(g2 * MP + c) * 2 + 1];
+      }
+      a.part[(size_t)blockIdx.x * 2 * MP + c] = t1;
+      a.part[(size_t)blockIdx.x * 2 * MP + MP + c] = t2;
     }
   }
   tcf_before();
@@ -603,7 +600,8 @@ bool update_tc3_supported(int w, int mp, int ld) {
 
 template <int MP>
 static void launch_tc3(mg_ctx *ctx, int grid, const CUtensorMap &mS, const CUtensorMap &mA,
-                       const CUtensorMap &mXS, const CUtensorMap &mXA, float *S, float *AS, const float *b, const float *prec, const float *Mg,
+                       const CUtensorMap &mXS, const CUtensorMap &mXA, const CUtensorMap &mOS,
+                       const CUtensorMap &mOA, const CUtensorMap &mOW, float *S, float *AS, const float *b, const float *prec, const float *Mg,
                        const double *theta, const Upd3Args &a) {
   constexpr size_t smem = u3_smem((3 * MP + 31) / 32, MP);
   static_assert(smem <= 227 * 1024, "tc update: shared memory");
@@ -613,8 +611,8 @@ static void launch_tc3(mg_ctx *ctx, int grid, const CUtensorMap &mS, const CUten
                                  (int)smem));
     attr_set = true;
   }
-  k_update_tc3<MP><<<grid, kU3Threads, smem, ctx->stream>>>(mS, mA, mXS, mXA, S, AS, b, prec, Mg,
-                                                            theta, a);
+  k_update_tc3<MP><<<grid, kU3Threads, smem, ctx->stream>>>(mS, mA, mXS, mXA, mOS, mOA, mOW, S, AS,
+                                                            b, prec, Mg, theta, a);
 }
 
 // one fast-path update on the tensor cores; part: [grid][2 mp]; returns the grid
@@ -641,9 +639,16 @@ int update_tc3(mg_ctx *ctx, int64_t n, int ld, int w, int m, int mp, float *S, f
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ctx->num_sms));
   const CUtensorMap mS = make_map_k(S, n, ld, w), mA = make_map_k(AS, n, ld, w);
   const CUtensorMap mXS = make_map_x(S, n, ld, mp, mp), mXA = make_map_x(AS, n, ld, mp, mp);
-  if (mp == 12) launch_tc3<12>(ctx, grid, mS, mA, mXS, mXA, S, AS, b, prec, Mg, theta, a);
-  else if (mp == 20) launch_tc3<20>(ctx, grid, mS, mA, mXS, mXA, S, AS, b, prec, Mg, theta, a);
-  else launch_tc3<36>(ctx, grid, mS, mA, mXS, mXA, S, AS, b, prec, Mg, theta, a);
+  // outputs: [X P W] of S, [AX AP] of AS, compact W (16-row boxes of complete rows)
+  const CUtensorMap mOS = make_map_x(S, n, ld, 3 * mp, 3 * mp);
+  const CUtensorMap mOA = make_map_x(AS, n, ld, 2 * mp, 2 * mp);
+  const CUtensorMap mOW = make_map_x(wc, n, mp, mp, mp);
+  if (mp == 12)
+    launch_tc3<12>(ctx, grid, mS, mA, mXS, mXA, mOS, mOA, mOW, S, AS, b, prec, Mg, theta, a);
+  else if (mp == 20)
+    launch_tc3<20>(ctx, grid, mS, mA, mXS, mXA, mOS, mOA, mOW, S, AS, b, prec, Mg, theta, a);
+  else
+    launch_tc3<36>(ctx, grid, mS, mA, mXS, mXA, mOS, mOA, mOW, S, AS, b, prec, Mg, theta, a);
   MG_CHECK_LAUNCH(ctx);
   return grid;
 }

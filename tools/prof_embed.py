@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--max-iter", type=int, default=None)
     ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--k", type=int, default=0, help="embedding dimension (default: the config's)")
     ap.add_argument("--stats", action="store_true", help="per-class CUDA-event kernel times")
     ap.add_argument("--morton", action="store_true",
                     help="experiment: number the points in Morton order of their coordinates "
@@ -42,7 +43,7 @@ def main():
         os.environ["MG_REORDER"] = "0"
     else:
         n, ptr, idx, w = synthetic.config_graph(cfg.name, n=args.n)
-    K = cfg.k
+    K = args.k or cfg.k
     scfg = mg.SolverConfig(k=K + 1, tol=cfg.tol, max_iter=args.max_iter or cfg.max_iter, seed=args.seed,
                            precision=cfg.precision)
     zh = np.random.default_rng(args.seed).standard_normal(core._stream_size(n, max(K + 1, 8)))
