@@ -33,6 +33,51 @@
 
 namespace mg {
 
+// Gram blocks of the updated [X | P] from the previous step's Gram matrices:
+// the update wrote [X P]_new = S_old T with T = [Zp + [Yx; 0; 0] | Zp] (and the
+// same T on the A-images), so G_new[XP, XP] = T' G_old T for both Grams.
+// Step 1: U_g = G_g T (w x 2mp), step 2: G_g[XP, XP] = T' U_g.  tc: the
+// coefficients as the tensor-core update applies them (TF32-rounded corrections).
+__device__ __forceinline__ double derive_T(const float *Mg, int w, int mp, int k, int a, int tc) {
+  const int c = a < mp ? a : a - mp;
+  const float zp = Mg[k * mp + c];
+  if (a >= mp) return tc ? (double)__uint_as_float((__float_as_uint(zp) + 0x1000u) & 0xFFFFE000u) : (double)zp;
+  if (k >= mp) return tc ? (double)__uint_as_float((__float_as_uint(zp) + 0x1000u) & 0xFFFFE000u) : (double)zp;
+  const float yx = Mg[w * mp + k * mp + c];
+  if (!tc) return (double)zp + (double)yx;
+  const float v = zp + (yx - (k == c ? 1.f : 0.f));
+  return (double)__uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u) + (k == c ? 1.0 : 0.0);
+}
+__global__ void k_gram_derive1(const double *__restrict__ G0, const double *__restrict__ G1,
+                               const float *__restrict__ Mg, int w, int mp, int tc,
+                               double *__restrict__ U) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x, g = blockIdx.y;
+  if (e >= w * 2 * mp) return;
+  const int k = e / (2 * mp), a = e - k * 2 * mp;
+  const double *G = g ? G1 : G0;
+  double s = 0.0;
+  for (int l = 0; l < w; ++l) s = fma(G[k * w + l], derive_T(Mg, w, mp, l, a, tc), s);
+  U[(size_t)g * w * 2 * mp + e] = s;
+}
+__global__ void k_gram_derive2(const double *__restrict__ U, const float *__restrict__ Mg, int w,
+                               int mp, int tc, double *__restrict__ G0, double *__restrict__ G1,
+                               double *__restrict__ dbg) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x, g = blockIdx.y;
+  if (e >= 4 * mp * mp) return;
+  const int a = e / (2 * mp), b = e - a * 2 * mp;
+  const double *Ug = U + (size_t)g * w * 2 * mp;
+  double s = 0.0;
+  for (int k = 0; k < w; ++k) s = fma(derive_T(Mg, w, mp, k, a, tc), Ug[k * 2 * mp + b], s);
+  double *G = g ? G1 : G0;
+  if (dbg) {  // largest |derived - computed| and largest |computed| per Gram (bit patterns: values >= 0)
+    atomicMax(reinterpret_cast<unsigned long long *>(dbg + 2 * g),
+              (unsigned long long)__double_as_longlong(fabs(s - G[a * w + b])));
+    atomicMax(reinterpret_cast<unsigned long long *>(dbg + 2 * g + 1),
+              (unsigned long long)__double_as_longlong(fabs(G[a * w + b])));
+  }
+  G[a * w + b] = s;
+}
+
 // debug (MG_UPD_TC_CHECK): per column block of width mp, max |a - b| and max |b|
 __global__ void k_upd_cmp(const float *__restrict__ a, const float *__restrict__ b, int64_t n,
                           int ld, int mp, int nblk, float *out) {
@@ -1444,6 +1489,9 @@ struct Lobpcg {
 
   int tk_gram = 32, ns_gram = 3, tk_upd = 32, rt_upd = 8;
   bool upd_ws = false;
+  bool tc_update_used = false;  // some update of this solve ran on the tensor cores
+  bool gram_prev_valid = false, refreshed_now = false, prev_update_tc = false;
+  DBuf<double> GBp, GAp, Uder;
   int tk_ws = 0;
   size_t ws_smem = 0;
 
@@ -1594,6 +1642,37 @@ struct Lobpcg {
   gram_done:
     ar(Gr0.p, (size_t)w * w);
     ar(Gr1.p, (size_t)w * w);
+    {
+      // experiment (MG_GRAM_DERIVE): [X P] x [X P] blocks from the previous Grams
+      static const int derive = (int)env_double("MG_GRAM_DERIVE", 0);
+      if (derive && sizeof(T) == 4) {
+        if (GBp.n < (size_t)w * w) {
+          GBp.alloc(ctx, (size_t)w * w);
+          GAp.alloc(ctx, (size_t)w * w);
+          Uder.alloc(ctx, (size_t)2 * w * 2 * mp + 8);
+        }
+        if (gram_prev_valid && !refreshed_now) {
+          double *dbg = (derive & 2) ? Uder.p + (size_t)2 * w * 2 * mp : nullptr;
+          if (dbg) MG_CUDA(cudaMemsetAsync(dbg, 0, 4 * sizeof(double), ctx->stream));
+          dim3 g1((w * 2 * mp + 127) / 128, 2), g2((4 * mp * mp + 127) / 128, 2);
+          k_gram_derive1<<<g1, 128, 0, ctx->stream>>>(GBp.p, GAp.p, (const float *)M.p, w, mp,
+                                                      prev_update_tc ? 1 : 0, Uder.p);
+          MG_CHECK_LAUNCH(ctx);
+          k_gram_derive2<<<g2, 128, 0, ctx->stream>>>(Uder.p, (const float *)M.p, w, mp,
+                                                      prev_update_tc ? 1 : 0, Gr0.p, Gr1.p, dbg);
+          MG_CHECK_LAUNCH(ctx);
+          if (dbg && (iter_now % 20) == 3) {
+            double h[4];
+            d2h_sync(ctx, h, dbg, sizeof(h));
+            fprintf(stderr, "[derive it=%d] GB diff %.2e / %.2e  GA diff %.2e / %.2e\n", iter_now,
+                    h[0], h[1], h[2], h[3]);
+          }
+        }
+        MG_CUDA(cudaMemcpyAsync(GBp.p, Gr0.p, (size_t)w * w * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        MG_CUDA(cudaMemcpyAsync(GAp.p, Gr1.p, (size_t)w * w * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        gram_prev_valid = false;  // set again below once this step's update has run
+      }
+    }
     FastArgs fa{};
     fa.m = m;
     fa.mp = mp;
@@ -1636,7 +1715,9 @@ struct Lobpcg {
       ProfScope ps(ctx, PROF_UPDATE, 2.0 * n * ld * sizeof(T) + 5.0 * n * mp * sizeof(T));
       const T *pr = sp.jacobi ? prec.p : nullptr;
       if constexpr (sizeof(T) == 4) {
-        static const int upd_tc = (int)env_double("MG_UPD_TC", 0);
+        // tcgen05 update for the widest blocks (w = 3mp > 96: K = 32); narrower
+        // blocks are faster on the CUDA cores (C3: 163 vs 305 us per launch)
+        static const int upd_tc = (int)env_double("MG_UPD_TC", 96);
         static const int upd_tc_check = (int)env_double("MG_UPD_TC_CHECK", 0);
         if (upd_tc && upd_tc_check && upd_ws && update_tc3_supported(w, mp, ld) &&
             (iter_now % upd_tc_check) == (upd_tc_check > 1 ? 1 : 0)) {
@@ -1681,6 +1762,8 @@ struct Lobpcg {
           goto upd_done;
         }
         if (upd_tc && !ua.emul && update_tc3_supported(w, mp, ld) && w > upd_tc) {
+          tc_update_used = true;
+          prev_update_tc = true;
           nblk_upd = update_tc3(ctx, n, ld, w, m, mp, (float *)S.p, (float *)AS.p,
                                 (const float *)bw.p, (const float *)pr, (const float *)M.p,
                                 theta.p, status.p + 5, colpart.p, (float *)Wc.p);
@@ -1689,6 +1772,7 @@ struct Lobpcg {
         if (upd_ws && !ua.emul) {
           UpdArgs uw = ua;
           uw.tk = tk_ws;
+          prev_update_tc = false;
           k_update_ws<4><<<grid_upd, kWsF + kWsS, ws_smem, ctx->stream>>>(
               (float *)S.p, (float *)AS.p, (const float *)bw.p, (const float *)pr,
               (const float *)M.p, theta.p, uw);
@@ -1863,7 +1947,21 @@ struct Lobpcg {
       res.history.push_back(ts);
       if (all) {  // re-verify against a fresh product (eigensolver.py:227-234)
         std::vector<double> th2;
+        if (tc_update_used) {
+          // The tensor-core update applies TF32-rounded coefficients: X leaves a
+          // step B-orthonormal only to ~2^-12 x the size of that step's rotation
+          // (the next step's re-orthonormalisation absorbs it).  Before the block
+          // is accepted it is B-orthonormalised and Rayleigh-Ritz-rotated exactly
+          // once (the initial block's procedure, eigensolver.py:196-200), so the
+          // returned pairs meet the fp32 bars on their own.
+          spmm_cols(0, mp);
+          orth_refill_rr(m);
+          pcount = 0;
+          tc_update_used = false;
+          gram_prev_valid = false;
+        }
         fresh_theta(th2);
+        gram_prev_valid = false;  // AX was just replaced by a fresh product
         iterate_sync(true, cr, th, st);
         if (conv_test(rn, cv)) break;
       }
@@ -1877,6 +1975,7 @@ struct Lobpcg {
         MG_CHECK_LAUNCH(ctx);
       }
       const bool prefix = (it % 32) != 0;
+      refreshed_now = sizeof(T) == 4 && (it % refresh_period()) == 0;
       if (sizeof(T) == 4 && (it % refresh_period()) == 0) {
         // fp32: carried A-images drift at fp32 resolution; refresh [AX AP AW]
         // with one wide SpMM at every full re-orthonormalisation
@@ -1916,6 +2015,7 @@ struct Lobpcg {
       // (MG_FULL_SWEEP=1 restores it for every 32nd iteration).
       static const bool robust_sweep = env_double("MG_FULL_SWEEP", 0) != 0;
       if (fast_ok && (prefix || !robust_sweep)) done = fast_iteration(vcols, cr, th, st);
+      gram_prev_valid = done;  // an accepted fast step: [X P]_new = S_old T, the saved Grams apply
       if (!done) {
         if (prefix) {
           for (int rep = 0; rep < 2; ++rep) {
@@ -1961,6 +2061,7 @@ struct Lobpcg {
       }
       pcount = m;
       if (st[1] < m) {  // basis collapsed (eigensolver.py:260-266)
+        gram_prev_valid = false;
         orth_refill_rr(st[1]);
         pcount = 0;
         iterate_sync(true, cr, th, st);
@@ -1969,6 +2070,11 @@ struct Lobpcg {
     if (it > sp.max_iter) it = sp.max_iter;
     res.iterations = it;
     // ---- honest final report (eigensolver.py:268-283)
+    if (tc_update_used) {  // budget exhausted after a tensor-core step: same exact finish
+      spmm_cols(0, mp);
+      orth_refill_rr(m);
+      tc_update_used = false;
+    }
     fresh_theta(th);
     iterate_sync(false, cr, th, st);
     conv_test(rn, cv);
