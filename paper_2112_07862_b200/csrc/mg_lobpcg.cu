@@ -78,6 +78,20 @@ __global__ void k_gram_derive2(const double *__restrict__ U, const float *__rest
   G[a * w + b] = s;
 }
 
+// debug: largest |a - b| relative to the entries' diagonal scale sqrt(|b_ii b_jj|),
+// separately for the [0, nxp) x [0, nxp) block (out[0]) and the rest (out[1])
+__global__ void k_gram_cmp(const double *__restrict__ a, const double *__restrict__ b, int w,
+                           int nxp, double *out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= w * w) return;
+  const int i = e / w, j = e - i * w;
+  const double sc = sqrt(fabs(b[i * w + i] * b[j * w + j]));
+  if (!(sc > 0.0)) return;
+  const double d = fabs(a[e] - b[e]) / sc;
+  atomicMax(reinterpret_cast<unsigned long long *>(out + ((i < nxp && j < nxp) ? 0 : 1)),
+            (unsigned long long)__double_as_longlong(d));
+}
+
 // debug (MG_UPD_TC_CHECK): per column block of width mp, max |a - b| and max |b|
 __global__ void k_upd_cmp(const float *__restrict__ a, const float *__restrict__ b, int64_t n,
                           int ld, int mp, int nblk, float *out) {
@@ -1491,6 +1505,8 @@ struct Lobpcg {
   bool upd_ws = false;
   bool tc_update_used = false;  // some update of this solve ran on the tensor cores
   bool gram_prev_valid = false, refreshed_now = false, prev_update_tc = false;
+  bool gram_narrow_now = false, safe_mode = false;
+  int gram_derive_mode = 0;  // MG_GRAM_DERIVE: 1 narrow Gram + derived [X P] blocks, |2 debug
   DBuf<double> GBp, GAp, Uder;
   int tk_ws = 0;
   size_t ws_smem = 0;
@@ -1601,6 +1617,7 @@ struct Lobpcg {
     const int w = 3 * mp;
     gpart.alloc(ctx, (size_t)grid_fast * 2 * w * w);
     use_tc = sizeof(T) == 4 && gram_tc_supported(w) && env_double("MG_TC_GRAM", 1) != 0;
+    gram_derive_mode = use_tc ? (int)env_double("MG_GRAM_DERIVE", 0) : 0;
     fast_ok = true;
   }
 
@@ -1619,8 +1636,21 @@ struct Lobpcg {
     const int total = 2 * ga.nsym;
     if constexpr (sizeof(T) == 4) {
       if (use_tc) {
-        gram_pair_tc(ctx, n, ld, w, (const float *)S.p, (const float *)AS.p,
+        // W-column blocks only when the [X P] blocks follow from the previous
+        // step (accepted fast step, no A-image refresh in between)
+        gram_narrow_now = gram_derive_mode && !safe_mode && gram_prev_valid && !refreshed_now &&
+                          gram_w_tc2_supported(w, mp, ld);
+        if (gram_derive_mode && GBp.n < (size_t)w * w) {
+          GBp.alloc(ctx, (size_t)w * w);
+          GAp.alloc(ctx, (size_t)w * w);
+          Uder.alloc(ctx, (size_t)2 * w * 2 * mp + 8);
+        }
+        if (gram_narrow_now)
+          gram_w_tc2(ctx, n, ld, w, mp, (const float *)S.p, (const float *)AS.p,
                      (const float *)bw.p, Gr0.p, Gr1.p, tcpart);
+        else
+          gram_pair_tc(ctx, n, ld, w, (const float *)S.p, (const float *)AS.p,
+                       (const float *)bw.p, Gr0.p, Gr1.p, tcpart);
         goto gram_done;
       }
     }
@@ -1642,36 +1672,33 @@ struct Lobpcg {
   gram_done:
     ar(Gr0.p, (size_t)w * w);
     ar(Gr1.p, (size_t)w * w);
-    {
-      // experiment (MG_GRAM_DERIVE): [X P] x [X P] blocks from the previous Grams
-      static const int derive = (int)env_double("MG_GRAM_DERIVE", 0);
-      if (derive && sizeof(T) == 4) {
-        if (GBp.n < (size_t)w * w) {
-          GBp.alloc(ctx, (size_t)w * w);
-          GAp.alloc(ctx, (size_t)w * w);
-          Uder.alloc(ctx, (size_t)2 * w * 2 * mp + 8);
-        }
-        if (gram_prev_valid && !refreshed_now) {
-          double *dbg = (derive & 2) ? Uder.p + (size_t)2 * w * 2 * mp : nullptr;
-          if (dbg) MG_CUDA(cudaMemsetAsync(dbg, 0, 4 * sizeof(double), ctx->stream));
-          dim3 g1((w * 2 * mp + 127) / 128, 2), g2((4 * mp * mp + 127) / 128, 2);
-          k_gram_derive1<<<g1, 128, 0, ctx->stream>>>(GBp.p, GAp.p, (const float *)M.p, w, mp,
-                                                      prev_update_tc ? 1 : 0, Uder.p);
-          MG_CHECK_LAUNCH(ctx);
-          k_gram_derive2<<<g2, 128, 0, ctx->stream>>>(Uder.p, (const float *)M.p, w, mp,
-                                                      prev_update_tc ? 1 : 0, Gr0.p, Gr1.p, dbg);
-          MG_CHECK_LAUNCH(ctx);
-          if (dbg && (iter_now % 20) == 3) {
-            double h[4];
-            d2h_sync(ctx, h, dbg, sizeof(h));
-            fprintf(stderr, "[derive it=%d] GB diff %.2e / %.2e  GA diff %.2e / %.2e\n", iter_now,
-                    h[0], h[1], h[2], h[3]);
-          }
-        }
-        MG_CUDA(cudaMemcpyAsync(GBp.p, Gr0.p, (size_t)w * w * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-        MG_CUDA(cudaMemcpyAsync(GAp.p, Gr1.p, (size_t)w * w * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-        gram_prev_valid = false;  // set again below once this step's update has run
+    if (gram_narrow_now) {
+      // [X P] x [X P] blocks of both Grams from the previous step's matrices
+      dim3 g1((w * 2 * mp + 127) / 128, 2), g2((4 * mp * mp + 127) / 128, 2);
+      k_gram_derive1<<<g1, 128, 0, ctx->stream>>>(GBp.p, GAp.p, (const float *)M.p, w, mp,
+                                                  prev_update_tc ? 1 : 0, Uder.p);
+      MG_CHECK_LAUNCH(ctx);
+      k_gram_derive2<<<g2, 128, 0, ctx->stream>>>(Uder.p, (const float *)M.p, w, mp,
+                                                  prev_update_tc ? 1 : 0, Gr0.p, Gr1.p, nullptr);
+      MG_CHECK_LAUNCH(ctx);
+      if (gram_derive_mode & 2) {  // debug: against the full Gram pair of the same block
+        DBuf<double> F0(ctx, (size_t)w * w), F1(ctx, (size_t)w * w), dd(ctx, 4);
+        dd.zero();
+        gram_pair_tc(ctx, n, ld, w, (const float *)S.p, (const float *)AS.p, (const float *)bw.p,
+                     F0.p, F1.p, tcpart);
+        k_gram_cmp<<<(w * w + 127) / 128, 128, 0, ctx->stream>>>(Gr0.p, F0.p, w, 2 * mp, dd.p);
+        k_gram_cmp<<<(w * w + 127) / 128, 128, 0, ctx->stream>>>(Gr1.p, F1.p, w, 2 * mp, dd.p + 2);
+        double h[4];
+        d2h_sync(ctx, h, dd.p, sizeof(h));
+        if ((iter_now % 20) == 3 || h[0] > 1e-4 || h[1] > 1e-4 || h[2] > 1e-4 || h[3] > 1e-4)
+          fprintf(stderr, "[gram narrow it=%d] rel diff vs full: GB xp %.2e w %.2e | GA xp %.2e w %.2e\n",
+                  iter_now, h[0], h[1], h[2], h[3]);
       }
+    }
+    if (gram_derive_mode && sizeof(T) == 4) {
+      MG_CUDA(cudaMemcpyAsync(GBp.p, Gr0.p, (size_t)w * w * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+      MG_CUDA(cudaMemcpyAsync(GAp.p, Gr1.p, (size_t)w * w * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+      gram_prev_valid = false;  // set again once this step's update has run
     }
     FastArgs fa{};
     fa.m = m;

@@ -22,6 +22,11 @@ bool gram_tc2_supported(int w, int ld);
 void gram_pair_tc2(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const float *AS,
                    const float *b, double *GB, double *GA, DBuf<double> &part);
 
+// narrow mode of the same kernel: only the W-column blocks of both Grams
+bool gram_w_tc2_supported(int w, int mp, int ld);
+void gram_w_tc2(mg_ctx *ctx, int64_t n, int ld, int w, int mp, const float *S, const float *AS,
+                const float *b, double *GB, double *GA, DBuf<double> &part);
+
 // tcgen05 update (mg_tc3.cu): P = S Zp, X += S (Zp + [Yx - I; 0; 0]) and the
 // A-images, fused residual / W / column norms; returns the grid (rows of part)
 bool update_tc3_supported(int w, int mp, int ld);

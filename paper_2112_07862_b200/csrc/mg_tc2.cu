@@ -146,7 +146,7 @@ __device__ __forceinline__ void split4(float4 x, float4 &hi, float4 &lo) {
 __device__ __forceinline__ void g2_drain(int fg, int NG, uint64_t *tmf, uint64_t *tme,
                                          uint32_t tbase, int q, int ch, int hw, int lane, int i,
                                          int jmin, int w, double *dp, float (&acc)[64],
-                                         bool skip) {
+                                         bool skip, bool full) {
   const int buf = fg & 1;
   mbar_wait(&tmf[buf], (fg >> 1) & 1);
   __syncwarp();
@@ -154,7 +154,7 @@ __device__ __forceinline__ void g2_drain(int fg, int NG, uint64_t *tmf, uint64_t
   const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + buf * 256 + ch * hw;
 #pragma unroll
   for (int c = 0; c < 64; c += 16) {
-    if (!skip && c < hw && ch * hw + c + 16 > 32 * q) {  // warp-uniform: block-lower chunks
+    if (!skip && c < hw && (full || ch * hw + c + 16 > 32 * q)) {  // warp-uniform: block-lower chunks
       float v[16], x[16];
       tmem_ld16_pair(ta + c, ta + 32 * (hw / 16) + c, v, x);
 #pragma unroll
@@ -168,7 +168,7 @@ __device__ __forceinline__ void g2_drain(int fg, int NG, uint64_t *tmf, uint64_t
 #pragma unroll
     for (int c = 0; c < 64; ++c) {
       const int j = ch * hw + c;
-      if (c < hw && j >= jmin && j < w && i < w) dp[(size_t)j * 128 + i] += (double)acc[c];
+      if (c < hw && j >= jmin && (full || j < w) && i < w) dp[(size_t)j * 128 + i] += (double)acc[c];
       acc[c] = 0.f;
     }
   }
@@ -180,6 +180,8 @@ struct Gram2TcArgs {
   int pwf;        // full panels (w / 32), loaded by the 3-D maps
   int npairs;     // grid = 2 * npairs
   int dbg;        // MG_TC2_DBG timing experiments: 1 no MMA, 2 no derive, 4 no drain
+  int narrow;     // 1: W-column blocks only (pw = 4, W = columns [72, 108)): every CTA owns
+                  // a row range and forms S' [bS(:, 64:128) | AS(:, 64:128)]
   double *part;   // [pair][h][128 (j)][128 (i)] fp64, zeroed by the host
 };
 
@@ -211,7 +213,8 @@ __global__ void __launch_bounds__(kG2Threads, 1)
   uint32_t *tslot = reinterpret_cast<uint32_t *>(tme + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int h = blockIdx.x & 1, pair = blockIdx.x >> 1;
+  const bool narrow = a.narrow != 0;
+  const int h = narrow ? 1 : (blockIdx.x & 1), pair = narrow ? blockIdx.x : (blockIdx.x >> 1);
   const int64_t ntiles = (a.n + kG2TK - 1) / kG2TK;
   const int64_t t0 = ntiles * pair / a.npairs, t1 = ntiles * (pair + 1) / a.npairs;
   const int T = (int)(t1 - t0);
@@ -248,13 +251,23 @@ __global__ void __launch_bounds__(kG2Threads, 1)
       if (h) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA3)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(
                        reinterpret_cast<uint64_t>(h ? &tmA : &tmB)) : "memory");
+      if (narrow) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
       for (int t = 0; t < T; ++t) {
         const int s = t % kG2Stages;
         mbar_wait(&empty[s], ((t / kG2Stages) & 1) ^ 1);
         unsigned char *st = sm + s * SB;
-        mbar_expect_tx(&full[s], h ? 2 * PB : PB + kG2TK * 4);
+        mbar_expect_tx(&full[s], narrow ? PB + 2 * kG2Panel + kG2TK * 4
+                                        : (h ? 2 * PB : PB + kG2TK * 4));
         const int r0 = (int)((t0 + t) * kG2TK);
-        if (!h) tma_1d(sb + s * 32, &tmB, r0, &full[s]);
+        if (!h || narrow) tma_1d(sb + s * 32, &tmB, r0, &full[s]);
+        if (narrow) {
+          // S: all panels (A side); AS: the two panels that hold the W block
+          tma_3d(st, &tmS3, r0, &full[s]);
+          for (int p = a.pwf; p < pw; ++p) tma_2d(st + p * kG2Panel, &tmS, 32 * p, r0, &full[s]);
+          tma_2d(st + 2 * PB + 2 * kG2Panel, &tmA, 64, r0, &full[s]);
+          tma_2d(st + 2 * PB + 3 * kG2Panel, &tmA, 96, r0, &full[s]);
+          continue;
+        }
         // full 32-column panels in one 3-D box, the partial last panel (zero
         // beyond w) as a 2-D box: 2 TMA instructions per matrix and tile
         if (a.pwf) {
@@ -308,7 +321,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
     const int nch = pw * kG2TK * 8;          // 16-byte chunks per pw-panel group
     const int i = 32 * q + lane;             // Gram row drained by this thread
     const int jmin = i & ~7;                 // block-upper part only
-    double *dp = a.part + ((size_t)pair * 2 + h) * 128 * 128;
+    double *dp = a.part + (narrow ? (size_t)pair : (size_t)pair * 2 + h) * 128 * 128;
     float acc[64];
 #pragma unroll
     for (int j = 0; j < 64; ++j) acc[j] = 0.f;
@@ -321,6 +334,23 @@ __global__ void __launch_bounds__(kG2Threads, 1)
         const int o = e * 16;
         const float4 x = *reinterpret_cast<const float4 *>(st + o);
         float4 hi, lo;
+        if (narrow) {
+          // panels 2, 3 of S also give B panels 0, 1 (b S); B panels 2, 3 are AS
+          if (o >= 2 * kG2Panel) {
+            const int ob = o - 2 * kG2Panel;
+            const float br = sb[s * 32 + ((o % kG2Panel) >> 7)];
+            split4(make_float4(br * x.x, br * x.y, br * x.z, br * x.w), hi, lo);
+            *reinterpret_cast<float4 *>(st + 2 * PB + ob) = hi;
+            *reinterpret_cast<float4 *>(st + 3 * PB + ob) = lo;
+            split4(*reinterpret_cast<const float4 *>(st + 2 * PB + o), hi, lo);
+            *reinterpret_cast<float4 *>(st + 2 * PB + o) = hi;
+            *reinterpret_cast<float4 *>(st + 3 * PB + o) = lo;
+          }
+          split4(x, hi, lo);
+          *reinterpret_cast<float4 *>(st + o) = hi;
+          *reinterpret_cast<float4 *>(st + PB + o) = lo;
+          continue;
+        }
         if (h == 0) {
           const float br = sb[s * 32 + ((o % kG2Panel) >> 7)];  // 0 beyond n (TMA fill)
           split4(make_float4(br * x.x, br * x.y, br * x.z, br * x.w), hi, lo);
@@ -338,11 +368,12 @@ __global__ void __launch_bounds__(kG2Threads, 1)
       if (lane == 0) arrive(&drv[s]);
       // drain group g two tiles after it closed (its MMAs have had time to finish)
       if (t % kG2FL == 1 && t > kG2FL)
-        g2_drain(drained++, NG, tmf, tme, tbase, q, ch, hw, lane, i, jmin, a.w, dp, acc,
-                 a.dbg & 4);
+        g2_drain(drained++, NG, tmf, tme, tbase, q, ch, hw, lane, i, narrow ? 0 : jmin, a.w, dp,
+                 acc, a.dbg & 4, narrow);
     }
     while (drained < NG)
-      g2_drain(drained++, NG, tmf, tme, tbase, q, ch, hw, lane, i, jmin, a.w, dp, acc, a.dbg & 4);
+      g2_drain(drained++, NG, tmf, tme, tbase, q, ch, hw, lane, i, narrow ? 0 : jmin, a.w, dp, acc,
+               a.dbg & 4, narrow);
   }
   tcf_before();
   __syncthreads();
@@ -434,6 +465,32 @@ CUtensorMap make_map_1d(const float *base, int64_t n) {
 
 }  // namespace
 
+// W-column blocks from the narrow kernel's partials: B column j < 64 is
+// G_B[i][64 + j], j >= 64 is G_A[i][j]; rows i < w, W columns [2mp, w).
+// Written with the full kernel's mirror convention (block-lower 8 x 8 blocks
+// come from the block-upper product), and mirrored into the W rows.
+__global__ void k_reduce_gram_w(const double *__restrict__ part, int nct, int w, int mp,
+                                double *__restrict__ GB, double *__restrict__ GA) {
+  const int nw = w - 2 * mp;
+  const int tot = 2 * w * nw;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
+    const int g = e / (w * nw);
+    const int r = e - g * w * nw;
+    int i = r / nw, j = 2 * mp + (r - i * nw);  // target entry (i, j), j a W column
+    const int ti = i, tj = j;
+    if ((i >> 3) > (j >> 3)) {  // block-lower inside the W x W block: take the mirror product
+      const int t = i;
+      i = j;
+      j = t;
+    }
+    double s = 0.0;
+    for (int c = 0; c < nct; ++c) s += part[((size_t)c * 128 + (g * 64 + j - 64)) * 128 + i];
+    double *G = g ? GA : GB;
+    G[ti * w + tj] = s;
+    if (ti < 2 * mp) G[tj * w + ti] = s;  // W rows x [X P] columns
+  }
+}
+
 bool gram_tc2_supported(int w, int ld) {
   return w > 32 && w <= 128 && ld % 4 == 0 && w % 4 == 0;
 }
@@ -477,6 +534,49 @@ void gram_pair_tc2(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const 
   }
   k_reduce_gram_tc2<<<grid_for(2 * w * w, 256, 4 * ctx->num_sms), 256, 0, ctx->stream>>>(
       part.p, npairs, w, GB, GA);
+  MG_CHECK_LAUNCH(ctx);
+}
+
+// W-column blocks only: G_B[:, W] = S' (b W), G_A[:, W] = S' (A W) and their
+// mirrors (rows W x columns [X P]); the [X P] x [X P] blocks are left untouched
+// (the caller derives them from the previous step's Grams).  w = 108 (mp = 36).
+bool gram_w_tc2_supported(int w, int mp, int ld) {
+  return gram_tc2_supported(w, ld) && (w + 31) / 32 == 4 && 2 * mp >= 64 && w == 3 * mp;
+}
+
+void gram_w_tc2(mg_ctx *ctx, int64_t n, int ld, int w, int mp, const float *S, const float *AS,
+                const float *b, double *GB, double *GA, DBuf<double> &part) {
+  require(gram_w_tc2_supported(w, mp, ld), MG_ERR_INTERNAL, "narrow tc2 Gram: unsupported width");
+  const int pw = 4;
+  const int64_t ntiles = (n + kG2TK - 1) / kG2TK;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ctx->num_sms));
+  const size_t need = (size_t)grid * 128 * 128;
+  if (part.n < need) part.alloc(ctx, need);
+  MG_CUDA(cudaMemsetAsync(part.p, 0, need * sizeof(double), ctx->stream));
+  Gram2TcArgs a{};
+  a.n = n;
+  a.w = w;
+  a.pw = pw;
+  a.npairs = grid;
+  a.part = part.p;
+  a.narrow = 1;
+  a.pwf = w / 32;
+  const CUtensorMap mS = make_map(S, n, ld, w), mA = make_map(AS, n, ld, w), mB = make_map_1d(b, n);
+  const CUtensorMap mS3 = make_map_3d(S, n, ld, a.pwf), mA3 = make_map_3d(AS, n, ld, a.pwf);
+  const size_t smem = g2_smem_bytes(pw);
+  static thread_local size_t smem_set = 0;
+  if (smem > smem_set) {
+    MG_CUDA(cudaFuncSetAttribute(k_gram_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    smem_set = smem;
+  }
+  {
+    ProfScope ps(ctx, PROF_GRAM, (double)n * (w + (w - 2 * mp)) * sizeof(float) + 4.0 * n);
+    k_gram_tc2<<<grid, kG2Threads, smem, ctx->stream>>>(mS, mA, mS3, mA3, mB, a);
+    MG_CHECK_LAUNCH(ctx);
+  }
+  k_reduce_gram_w<<<grid_for(2 * w * (w - 2 * mp), 256, 4 * ctx->num_sms), 256, 0, ctx->stream>>>(
+      part.p, grid, w, mp, GB, GA);
   MG_CHECK_LAUNCH(ctx);
 }
 
