@@ -1357,7 +1357,10 @@ struct Lobpcg {
     const char *e = getenv(name);
     return e ? atof(e) : dflt;
   }
-  static double rel_tol() { return sizeof(T) == 8 ? 1e-7 : env_double("MG_REL_TOL32", 1e-2); }
+  double rel_tol_scale = 1.0;  // raised after a second breakdown recovery
+  double rel_tol() const {
+    return sizeof(T) == 8 ? 1e-7 : rel_tol_scale * env_double("MG_REL_TOL32", 1e-2);
+  }
   // fp32: carried A-images drift ~1e-7 per transform and small pivots amplify
   // it, so [AX AP AW] is recomputed by one wide SpMM every `refresh` steps
   int refresh_period() const { return sizeof(T) == 8 ? 32 : (int)env_double("MG_REFRESH32", 16); }
@@ -1506,6 +1509,11 @@ struct Lobpcg {
   bool tc_update_used = false;  // some update of this solve ran on the tensor cores
   bool gram_prev_valid = false, refreshed_now = false, prev_update_tc = false;
   bool gram_narrow_now = false, safe_mode = false;
+  // fp32 breakdown recovery: two alternating copies of X, taken every 8 healthy
+  // iterations; restored (the older one) when the residuals blow up
+  DBuf<T> ckpt[2];
+  int ckpt_iter[2] = {-1, -1};
+  int recoveries = 0;
   int gram_derive_mode = 0;  // MG_GRAM_DERIVE: 1 narrow Gram + derived [X P] blocks, |2 debug
   DBuf<double> GBp, GAp, Uder;
   int tk_ws = 0;
@@ -1617,7 +1625,7 @@ struct Lobpcg {
     const int w = 3 * mp;
     gpart.alloc(ctx, (size_t)grid_fast * 2 * w * w);
     use_tc = sizeof(T) == 4 && gram_tc_supported(w) && env_double("MG_TC_GRAM", 1) != 0;
-    gram_derive_mode = use_tc ? (int)env_double("MG_GRAM_DERIVE", 0) : 0;
+    gram_derive_mode = use_tc ? (int)env_double("MG_GRAM_DERIVE", 1) : 0;
     fast_ok = true;
   }
 
@@ -1788,7 +1796,7 @@ struct Lobpcg {
                   nd);
           goto upd_done;
         }
-        if (upd_tc && !ua.emul && update_tc3_supported(w, mp, ld) && w > upd_tc) {
+        if (upd_tc && !safe_mode && !ua.emul && update_tc3_supported(w, mp, ld) && w > upd_tc) {
           tc_update_used = true;
           prev_update_tc = true;
           nblk_upd = update_tc3(ctx, n, ld, w, m, mp, (float *)S.p, (float *)AS.p,
@@ -1965,10 +1973,63 @@ struct Lobpcg {
     fast_setup();
     iterate_sync(true, cr, th, st);  // residual block of the initial Ritz vectors
     int it = 0;
+    // health of the fp32 trajectory: the largest squared residual norm of the
+    // block, against its minimum over the recent past
+    double h_min = 1e300;
+    const bool guard32 = sizeof(T) == 4 && fast_ok && env_double("MG_RECOVER", 1) != 0;
+    auto recover = [&](const char *why) {
+      // the older checkpoint predates the breakdown by >= 8 iterations
+      int slot = -1;
+      for (int q = 0; q < 2; ++q)
+        if (ckpt_iter[q] >= 0 && (slot < 0 || ckpt_iter[q] < ckpt_iter[slot])) slot = q;
+      require(slot >= 0 && recoveries < 3, MG_ERR_INTERNAL,
+              std::string("LOBPCG breakdown (") + why + ") at iteration " + std::to_string(it) +
+                  " and no checkpoint / too many recoveries");
+      ++recoveries;
+      if (env_double("MG_DEBUG_RECOVER", 0) != 0)
+        fprintf(stderr, "[recover] it=%d (%s): back to the block of iteration %d, safe mode %d\n", it,
+                why, ckpt_iter[slot], recoveries);
+      k_copy_cols<T><<<grid_for(n * mp, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          n, ckpt[slot].p, mp, 0, S.p, ld, 0, mp);
+      MG_CHECK_LAUNCH(ctx);
+      ckpt_iter[0] = ckpt_iter[1] = -1;
+      safe_mode = true;  // CUDA-core update, full Gram pair from here on
+      if (recoveries >= 2) rel_tol_scale = 3.0;
+      gram_prev_valid = false;
+      tc_update_used = false;
+      spmm_cols(0, mp);
+      orth_refill_rr(m);
+      pcount = 0;
+      iterate_sync(true, cr, th, st);
+      h_min = 1e300;
+    };
     for (it = 1; it <= sp.max_iter; ++it) {
       iter_now = it;
       debug_check("resid");
       bool all = conv_test(rn, cv);
+      if (guard32) {
+        double h = 0.0;
+        bool finite = true;
+        for (int c = 0; c < m; ++c) {
+          h = std::max(h, cr[c]);
+          finite = finite && std::isfinite(cr[c]) && std::isfinite(cr[mp + c]) && std::isfinite(th[c]);
+        }
+        if (!finite || h > 1e4 * h_min) {
+          recover(finite ? "residual norms grew 100x" : "non-finite residuals");
+          all = conv_test(rn, cv);
+        } else {
+          h_min = std::min(h_min * 1.5, h);  // forgets old minima slowly
+          if ((it & 7) == 1) {
+            const int slot = (it >> 3) & 1;
+            if (ckpt[slot].n < (size_t)n * mp) ckpt[slot].alloc(ctx, (size_t)n * mp);
+            k_copy_cols<T><<<grid_for(n * mp, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+                n, S.p, ld, 0, ckpt[slot].p, mp, 0, mp);
+            MG_CHECK_LAUNCH(ctx);
+            ckpt_iter[slot] = it;
+          }
+        }
+      }
+      try {
       double ts = 0.0;
       for (int c = 0; c < m; ++c) ts += th[c];
       res.history.push_back(ts);
@@ -2092,6 +2153,11 @@ struct Lobpcg {
         orth_refill_rr(st[1]);
         pcount = 0;
         iterate_sync(true, cr, th, st);
+      }
+      } catch (const Error &e) {
+        // a step that produced non-finite small matrices: same recovery
+        if (!guard32 || std::string(e.what()).find("non-finite") == std::string::npos) throw;
+        recover("non-finite Gram / Rayleigh-Ritz matrices");
       }
     }
     if (it > sp.max_iter) it = sp.max_iter;

@@ -154,7 +154,9 @@ __device__ __forceinline__ void g2_drain(int fg, int NG, uint64_t *tmf, uint64_t
   const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + buf * 256 + ch * hw;
 #pragma unroll
   for (int c = 0; c < 64; c += 16) {
-    if (!skip && c < hw && (full || ch * hw + c + 16 > 32 * q)) {  // warp-uniform: block-lower chunks
+    // warp-uniform: block-lower chunks are skipped (mirror convention); in the
+    // narrow mode (full) only B columns 8 .. 43 of each 64-column half are W columns
+    if (!skip && c < hw && (full ? c < 48 : ch * hw + c + 16 > 32 * q)) {
       float v[16], x[16];
       tmem_ld16_pair(ta + c, ta + 32 * (hw / 16) + c, v, x);
 #pragma unroll
