@@ -441,16 +441,36 @@ def main():
         if kname in st and st[kname]["launches"]:
             avg_s = st[kname]["ms"] / st[kname]["launches"] / 1e3
             if kname == "update":
-                flops = 2.0 * (w_blk * mp_blk + mp_blk * mp_blk) * 2 * n
-                rl["update"] = {"bound": "fp32-fma", "achieved": flops / avg_s / 1e12,
-                                "peak": 72.56, "unit": "TFLOP/s",
-                                "frac": flops / avg_s / 1e12 / 72.56,
-                                "hbm_frac": 10 * m_blk * 4 * n / avg_s / 1e9 / hbm}
+                tc_upd = w_blk > int(os.environ.get("MG_UPD_TC", "96")) > 0 and mp_blk in (12, 20, 36)
+                if tc_upd:
+                    # k_update_tc3: 2 TF32 MMAs (hi, lo rows) per k-step, M padded to
+                    # 128 output columns, K = w rounded to 8, both S and AS; HBM:
+                    # SURVEY 8(d) 10 m s_v N
+                    kpad = (w_blk + 7) // 8 * 8
+                    flops = 2.0 * 2 * 2 * 128 * kpad * n
+                    gbs = 10 * m_blk * 4 * n / avg_s / 1e9
+                    rl["update"] = {"kernel": "k_update_tc3 (tcgen05)", "bound": "hbm",
+                                    "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                                    "tensor_frac": flops / avg_s / 1e12 / (bf16 / 2),
+                                    "note": "class average incl. the CUDA-core launches of safe-mode / "
+                                            "narrow solves"}
+                else:
+                    flops = 2.0 * (w_blk * mp_blk + mp_blk * mp_blk) * 2 * n
+                    rl["update"] = {"kernel": "k_update_ws", "bound": "fp32-fma",
+                                    "achieved": flops / avg_s / 1e12,
+                                    "peak": 72.56, "unit": "TFLOP/s",
+                                    "frac": flops / avg_s / 1e12 / 72.56,
+                                    "hbm_frac": 10 * m_blk * 4 * n / avg_s / 1e9 / hbm}
             else:
+                # class average over the narrow launches (W-column blocks: S, the W
+                # block of AS and b are read: (w + mp) s_v N) and the full pair
+                # every refresh (SURVEY 8(d) 6 m s_v N); bytes as each launch recorded
+                gbs = st[kname]["bytes"] / (st[kname]["ms"] / 1e3) / 1e9
                 flops = 2.0 * 2 * 3 * 128 * 128 * n
-                rl["gram"] = {"bound": "tensor", "achieved": flops / avg_s / 1e12,
-                              "peak": bf16 / 2, "unit": "TFLOP/s", "frac": flops / avg_s / 1e12 / (bf16 / 2),
-                              "hbm_frac": 6 * m_blk * 4 * n / avg_s / 1e9 / hbm}
+                rl["gram"] = {"kernel": "k_gram_tc2 (tcgen05; narrow + derived [X P] blocks, "
+                                        "full pair at refreshes)", "bound": "hbm",
+                              "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                              "full_pair_tensor_frac_if_all_full": flops / avg_s / 1e12 / (bf16 / 2)}
     kern = {k: {"launches": v["launches"], "ms_per_step": v["ms"] / args.steps,
                 "avg_us": 1e3 * v["ms"] / max(v["launches"], 1),
                 "GB_per_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
