@@ -16,3 +16,11 @@ res, bt, dg = core.embed_arrays(*g, c.k, cfg)
 tight = z["tight_eigenvalues"][:c.k + 1]; ref = z["ref_eigenvalues"]
 rel = np.abs(res.eigenvalues - tight) / tight
 print("seed", seed, "iterations", res.iterations, "conv", bool(res.converged.all()), "max rel_t first29 %.2e last4 %s" % (rel[:29].max(), np.array2string(rel[-4:], precision=1)), "resid last4", np.array2string(np.asarray(res.residual_norms[-4:]), precision=1))
+
+vecs = res.eigenvectors.cpu().numpy(); b = bt.cpu().numpy()
+V = z["tight_eigenvectors"].astype(np.float64)
+out = []
+for cl, ra in zip(meta["clusters"]["complete"], meta["clusters"]["ref_angle_per_cluster"]):
+    ang = float(tsp.principal_angles(vecs[:, cl], V[:, cl], b).max())
+    out.append("%.1f" % (ang / ra))
+print("angle / reference angle per complete cluster:", " ".join(out))
