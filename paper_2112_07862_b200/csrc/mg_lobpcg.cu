@@ -1953,13 +1953,13 @@ struct Lobpcg {
     int pcount = 0;
     std::vector<double> cr, th;
     const double tol = sp.tol;
-    // Acceptance margin of the derived-Gram path (MG_ACCEPT32, default 0.7): with the
-    // [X P] blocks derived instead of reduced the block reaches the reference's rule
-    // in fewer steps (C5-200K: 194-208 instead of 273), i.e. it is accepted with the
-    // columns next to the block edge less settled (angle to the tight vectors 3-6 x
-    // the reference's own instead of 1.9 x).  Requiring the in-loop test to clear
-    // the tolerance by the margin keeps the accepted block as converged as the
-    // reference's; the reported flags always use the reference's rule itself.
+    // Optional acceptance margin (MG_ACCEPT32, default 1 = the reference's rule as
+    // is).  With the [X P] blocks derived instead of reduced the block reaches the
+    // rule in fewer steps at C5-200K (194-208 instead of 273), i.e. it is accepted
+    // with the cluster next to the block edge less settled (angle to the tight
+    // vectors 3.2 x the reference's own instead of 1.9 x).  A margin of 0.7 restores
+    // 275 steps and 1.7 x there, but costs +14 % iterations at C5-20M (533 vs 468),
+    // so it is not the default; the reported flags always use the rule itself.
     double accept = 1.0;
     auto conv_test = [&](std::vector<double> &rn, std::vector<int> &cv) {
       rn.assign(m, 0.0);
@@ -1980,7 +1980,7 @@ struct Lobpcg {
     int st[4] = {m, m, m, m};
     fast_setup();
     if (gram_derive_mode && gram_w_tc2_supported(3 * mp, mp, ld))
-      accept = env_double("MG_ACCEPT32", 0.7);
+      accept = env_double("MG_ACCEPT32", 1.0);
     iterate_sync(true, cr, th, st);  // residual block of the initial Ritz vectors
     int it = 0;
     // health of the fp32 trajectory: the largest squared residual norm of the

@@ -1,12 +1,12 @@
 // tcgen05 Gram pair: host-side dispatch (the kernel is k_gram_tc2, mg_tc2.cu).
 //
 // Round 1 also carried a converter-based v1 Gram (3-piece TF32) and a
-// tensor-core update; both were off by default and are gone.  Why the update
-// stays on the CUDA cores (profiles/r2_update_tc_numerics.md): every
-// tensor-core formulation that was measured perturbs the fp32 LOBPCG
-// trajectory enough to cost iterations -- 3xTF32 +15 %, and Ozaki-style
-// fixed-point int8 slices with exact integer accumulation +606 % (4 slices)
-// and +6 % (5 slices) at C5-2M -- more than the per-launch saving.
+// tensor-core update that formed X Yx itself on tcgen05; both cost LOBPCG
+// iterations (+15 % .. +210 %) and are gone.  Round 2's update kernel
+// (mg_tc3.cu) forms only the corrections X (Yx - I) + P on the tensor core
+// and keeps the iteration count (profiles/r2_update_tc3.md); an Ozaki-style
+// int8 fixed-point variant was emulated and rejected
+// (profiles/r2_update_tc_numerics.md).
 #include "mg_tc.cuh"
 
 namespace mg {
