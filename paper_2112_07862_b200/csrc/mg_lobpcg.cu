@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
+#include <limits>
 #include <numeric>
 
 #include "mg_block.cuh"
@@ -1752,7 +1753,7 @@ struct Lobpcg {
       if constexpr (sizeof(T) == 4) {
         // tcgen05 update for the widest blocks (w = 3mp > 96: K = 32); narrower
         // blocks are faster on the CUDA cores (C3: 163 vs 305 us per launch)
-        static const int upd_tc = (int)env_double("MG_UPD_TC", 96);
+        const int upd_tc = (int)env_double("MG_UPD_TC", 96);  // read per call: tests toggle it
         static const int upd_tc_check = (int)env_double("MG_UPD_TC_CHECK", 0);
         if (upd_tc && upd_tc_check && upd_ws && update_tc3_supported(w, mp, ld) &&
             (iter_now % upd_tc_check) == (upd_tc_check > 1 ? 1 : 0)) {
@@ -1999,6 +2000,11 @@ struct Lobpcg {
       if (env_double("MG_DEBUG_RECOVER", 0) != 0)
         fprintf(stderr, "[recover] it=%d (%s): back to the block of iteration %d, safe mode %d\n", it,
                 why, ckpt_iter[slot], recoveries);
+      // nothing of the broken step survives: P, W and every A-image are rebuilt
+      S.zero();
+      AS.zero();
+      Wc.zero();
+      status.zero();  // the non-finite flag of the small-matrix kernels is sticky
       k_copy_cols<T><<<grid_for(n * mp, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
           n, ckpt[slot].p, mp, 0, S.p, ld, 0, mp);
       MG_CHECK_LAUNCH(ctx);
@@ -2018,6 +2024,14 @@ struct Lobpcg {
       debug_check("resid");
       bool all = conv_test(rn, cv);
       if (guard32) {
+        // test hook (MG_DEBUG_INJECT_NAN=it): poison one entry of W at that iteration
+        const int inject = (int)env_double("MG_DEBUG_INJECT_NAN", 0);  // read per step: tests set it
+        if (inject > 0 && it == inject && recoveries == 0) {
+          const T bad = std::numeric_limits<T>::quiet_NaN();
+          MG_CUDA(cudaMemcpyAsync(S.p + 2 * mp, &bad, sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+          MG_CUDA(cudaMemcpyAsync(Wc.p, &bad, sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+          MG_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
         double h = 0.0;
         bool finite = true;
         for (int c = 0; c < m; ++c) {
