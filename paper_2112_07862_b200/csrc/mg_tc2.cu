@@ -146,7 +146,7 @@ __device__ __forceinline__ void split4(float4 x, float4 &hi, float4 &lo) {
 __device__ __forceinline__ void g2_drain(int fg, int NG, uint64_t *tmf, uint64_t *tme,
                                          uint32_t tbase, int q, int ch, int hw, int lane, int i,
                                          int jmin, int w, double *dp, float (&acc)[64],
-                                         bool skip, bool full) {
+                                         bool skip, bool full, int wneed) {
   const int buf = fg & 1;
   mbar_wait(&tmf[buf], (fg >> 1) & 1);
   __syncwarp();
@@ -156,7 +156,7 @@ __device__ __forceinline__ void g2_drain(int fg, int NG, uint64_t *tmf, uint64_t
   for (int c = 0; c < 64; c += 16) {
     // warp-uniform: block-lower chunks are skipped (mirror convention); in the
     // narrow mode (full) only B columns 8 .. 43 of each 64-column half are W columns
-    if (!skip && c < hw && (full ? c < 48 : ch * hw + c + 16 > 32 * q)) {
+    if (!skip && c < hw && (full ? c < wneed : ch * hw + c + 16 > 32 * q)) {
       float v[16], x[16];
       tmem_ld16_pair(ta + c, ta + 32 * (hw / 16) + c, v, x);
 #pragma unroll
@@ -182,8 +182,11 @@ struct Gram2TcArgs {
   int pwf;        // full panels (w / 32), loaded by the 3-D maps
   int npairs;     // grid = 2 * npairs
   int dbg;        // MG_TC2_DBG timing experiments: 1 no MMA, 2 no derive, 4 no drain
-  int narrow;     // 1: W-column blocks only (pw = 4, W = columns [72, 108)): every CTA owns
-                  // a row range and forms S' [bS(:, 64:128) | AS(:, 64:128)]
+  int narrow;     // 1: W-column blocks only: every CTA owns a row range and forms
+                  // S' [bS(:, 32 pw0:) | AS(:, 32 pw0:)] with pw0 = pw / 2 (the panels that
+                  // hold W: pw = 4, mp = 36: columns [72, 108) in panels 2-3; pw = 2,
+                  // mp = 20: columns [40, 60) in panel 1)
+  int wneed;      // narrow: B columns of each half that are drained (multiple of 16)
   double *part;   // [pair][h][128 (j)][128 (i)] fp64, zeroed by the host
 };
 
@@ -258,16 +261,16 @@ __global__ void __launch_bounds__(kG2Threads, 1)
         const int s = t % kG2Stages;
         mbar_wait(&empty[s], ((t / kG2Stages) & 1) ^ 1);
         unsigned char *st = sm + s * SB;
-        mbar_expect_tx(&full[s], narrow ? PB + 2 * kG2Panel + kG2TK * 4
+        mbar_expect_tx(&full[s], narrow ? PB + (pw - pw / 2) * kG2Panel + kG2TK * 4
                                         : (h ? 2 * PB : PB + kG2TK * 4));
         const int r0 = (int)((t0 + t) * kG2TK);
         if (!h || narrow) tma_1d(sb + s * 32, &tmB, r0, &full[s]);
         if (narrow) {
-          // S: all panels (A side); AS: the two panels that hold the W block
-          tma_3d(st, &tmS3, r0, &full[s]);
+          // S: all panels (A side); AS: the panels that hold the W block
+          if (a.pwf) tma_3d(st, &tmS3, r0, &full[s]);
           for (int p = a.pwf; p < pw; ++p) tma_2d(st + p * kG2Panel, &tmS, 32 * p, r0, &full[s]);
-          tma_2d(st + 2 * PB + 2 * kG2Panel, &tmA, 64, r0, &full[s]);
-          tma_2d(st + 2 * PB + 3 * kG2Panel, &tmA, 96, r0, &full[s]);
+          for (int p = pw / 2; p < pw; ++p)
+            tma_2d(st + 2 * PB + p * kG2Panel, &tmA, 32 * p, r0, &full[s]);
           continue;
         }
         // full 32-column panels in one 3-D box, the partial last panel (zero
@@ -337,9 +340,9 @@ __global__ void __launch_bounds__(kG2Threads, 1)
         const float4 x = *reinterpret_cast<const float4 *>(st + o);
         float4 hi, lo;
         if (narrow) {
-          // panels 2, 3 of S also give B panels 0, 1 (b S); B panels 2, 3 are AS
-          if (o >= 2 * kG2Panel) {
-            const int ob = o - 2 * kG2Panel;
+          // the upper panels of S also give the lower B panels (b S); the upper B panels are AS
+          if (o >= (pw / 2) * kG2Panel) {
+            const int ob = o - (pw / 2) * kG2Panel;
             const float br = sb[s * 32 + ((o % kG2Panel) >> 7)];
             split4(make_float4(br * x.x, br * x.y, br * x.z, br * x.w), hi, lo);
             *reinterpret_cast<float4 *>(st + 2 * PB + ob) = hi;
@@ -371,11 +374,11 @@ __global__ void __launch_bounds__(kG2Threads, 1)
       // drain group g two tiles after it closed (its MMAs have had time to finish)
       if (t % kG2FL == 1 && t > kG2FL)
         g2_drain(drained++, NG, tmf, tme, tbase, q, ch, hw, lane, i, narrow ? 0 : jmin, a.w, dp,
-                 acc, a.dbg & 4, narrow);
+                 acc, a.dbg & 4, narrow, a.wneed);
     }
     while (drained < NG)
       g2_drain(drained++, NG, tmf, tme, tbase, q, ch, hw, lane, i, narrow ? 0 : jmin, a.w, dp, acc,
-               a.dbg & 4, narrow);
+               a.dbg & 4, narrow, a.wneed);
   }
   tcf_before();
   __syncthreads();
@@ -467,11 +470,12 @@ CUtensorMap make_map_1d(const float *base, int64_t n) {
 
 }  // namespace
 
-// W-column blocks from the narrow kernel's partials: B column j < 64 is
-// G_B[i][64 + j], j >= 64 is G_A[i][j]; rows i < w, W columns [2mp, w).
+// W-column blocks from the narrow kernel's partials (hb = 32 pw / 2 columns per
+// half): B column j < hb is G_B[i][hb + j], j >= hb is G_A[i][j]; rows i < w,
+// W columns [2mp, w).
 // Written with the full kernel's mirror convention (block-lower 8 x 8 blocks
 // come from the block-upper product), and mirrored into the W rows.
-__global__ void k_reduce_gram_w(const double *__restrict__ part, int nct, int w, int mp,
+__global__ void k_reduce_gram_w(const double *__restrict__ part, int nct, int w, int mp, int hb,
                                 double *__restrict__ GB, double *__restrict__ GA) {
   const int nw = w - 2 * mp;
   const int tot = 2 * w * nw;
@@ -486,7 +490,7 @@ __global__ void k_reduce_gram_w(const double *__restrict__ part, int nct, int w,
       j = t;
     }
     double s = 0.0;
-    for (int c = 0; c < nct; ++c) s += part[((size_t)c * 128 + (g * 64 + j - 64)) * 128 + i];
+    for (int c = 0; c < nct; ++c) s += part[((size_t)c * 128 + (g * hb + j - hb)) * 128 + i];
     double *G = g ? GA : GB;
     G[ti * w + tj] = s;
     if (ti < 2 * mp) G[tj * w + ti] = s;  // W rows x [X P] columns
@@ -541,15 +545,16 @@ void gram_pair_tc2(mg_ctx *ctx, int64_t n, int ld, int w, const float *S, const 
 
 // W-column blocks only: G_B[:, W] = S' (b W), G_A[:, W] = S' (A W) and their
 // mirrors (rows W x columns [X P]); the [X P] x [X P] blocks are left untouched
-// (the caller derives them from the previous step's Grams).  w = 108 (mp = 36).
+// (the caller derives them from the previous step's Grams).  w = 108 (mp = 36) or w = 60 (mp = 20).
 bool gram_w_tc2_supported(int w, int mp, int ld) {
-  return gram_tc2_supported(w, ld) && (w + 31) / 32 == 4 && 2 * mp >= 64 && w == 3 * mp;
+  const int pw = (w + 31) / 32;
+  return gram_tc2_supported(w, ld) && pw % 2 == 0 && 2 * mp >= 32 * (pw / 2) && w == 3 * mp;
 }
 
 void gram_w_tc2(mg_ctx *ctx, int64_t n, int ld, int w, int mp, const float *S, const float *AS,
                 const float *b, double *GB, double *GA, DBuf<double> &part) {
   require(gram_w_tc2_supported(w, mp, ld), MG_ERR_INTERNAL, "narrow tc2 Gram: unsupported width");
-  const int pw = 4;
+  const int pw = (w + 31) / 32, hb = 32 * (pw / 2);
   const int64_t ntiles = (n + kG2TK - 1) / kG2TK;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ctx->num_sms));
   const size_t need = (size_t)grid * 128 * 128;
@@ -562,6 +567,7 @@ void gram_w_tc2(mg_ctx *ctx, int64_t n, int ld, int w, int mp, const float *S, c
   a.npairs = grid;
   a.part = part.p;
   a.narrow = 1;
+  a.wneed = (w - hb + 15) / 16 * 16;
   a.pwf = w / 32;
   const CUtensorMap mS = make_map(S, n, ld, w), mA = make_map(AS, n, ld, w), mB = make_map_1d(b, n);
   const CUtensorMap mS3 = make_map_3d(S, n, ld, a.pwf), mA3 = make_map_3d(AS, n, ld, a.pwf);
@@ -578,7 +584,7 @@ void gram_w_tc2(mg_ctx *ctx, int64_t n, int ld, int w, int mp, const float *S, c
     MG_CHECK_LAUNCH(ctx);
   }
   k_reduce_gram_w<<<grid_for(2 * w * (w - 2 * mp), 256, 4 * ctx->num_sms), 256, 0, ctx->stream>>>(
-      part.p, grid, w, mp, GB, GA);
+      part.p, grid, w, mp, hb, GB, GA);
   MG_CHECK_LAUNCH(ctx);
 }
 
