@@ -149,13 +149,21 @@ def embed_arrays_dist(comm: Comm, ctx, device: int, n, indptr, indices, weights,
     out.history_cap = hist.size
     dg = N.EmbedDiag()
     torch.cuda.synchronize(dev)
-    try:
-        N.call("mg_embed_dist", ctx, comm.handle, n, C.c_void_p(p.data_ptr()),
-               C.c_void_p(i.data_ptr()), C.c_void_p(w.data_ptr()), k, C.byref(s),
-               int(literal_diagonal), 0, int(check_connected), C.c_void_p(z.data_ptr()), nz,
-               C.c_void_p(P.data_ptr()), C.c_void_p(b.data_ptr()), C.byref(out), C.byref(dg))
-    except N.NativeError as e:
-        _core._raise_native(e)
+    # A short normal stream (the eps solve doubling its block, refills) fails with the
+    # same MG_ERR_INPUT on every rank: retry with a longer stream, like core.embed
+    for attempt in range(4):
+        try:
+            N.call("mg_embed_dist", ctx, comm.handle, n, C.c_void_p(p.data_ptr()),
+                   C.c_void_p(i.data_ptr()), C.c_void_p(w.data_ptr()), k, C.byref(s),
+                   int(literal_diagonal), 0, int(check_connected), C.c_void_p(z.data_ptr()), nz,
+                   C.c_void_p(P.data_ptr()), C.c_void_p(b.data_ptr()), C.byref(out), C.byref(dg))
+            break
+        except N.NativeError as e:
+            if "stream exhausted" in str(e) and attempt < 3 and device_inputs is None:
+                nz *= 8
+                z = _core._normals_on(device, cfg.seed, nz, ctx)
+                continue
+            _core._raise_native(e)
     res = EigenResult(eigenvalues=ev.copy(), eigenvectors=P[:n * m].view(n, m),
                       iterations=int(out.iterations), residual_norms=rn.copy(),
                       converged=cv.astype(bool), ritz_sum_history=list(hist[:out.history_len]))
