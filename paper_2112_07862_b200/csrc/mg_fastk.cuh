@@ -266,16 +266,7 @@ struct UpdArgs {
   const int *skip;        // device flag: nonzero -> return (fallback iteration)
   double *part;           // [grid][2*mp]
   void *wc;               // compact W copy (n x mp), the SpMM input
-  int emul;               // experiment: emulate a 2-piece TF32 tensor-core update (k_update_resid)
 };
-
-// TF32 pieces as the tensor core would see them (experiment only)
-__device__ __forceinline__ float emu_rn_tf32(float x) {
-  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-}
-__device__ __forceinline__ float emu_tr_tf32(float x) {
-  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-}
 
 template <typename T, int NS, int RT>
 __global__ void __launch_bounds__(kFThreads, 1)
@@ -388,55 +379,6 @@ __global__ void __launch_bounds__(kFThreads, 1)
           }
         }
         if constexpr (sizeof(T) == 4) {
-         if (a.emul) {
-          // emulated tensor-core arithmetic: hi*hi + hi*lo + lo*hi, TF32 pieces,
-          // accumulation rounded toward zero (bit 1) ; phase 1 forms the
-          // correction X (Yx - I) + P and adds the old X exactly (bit 2)
-          const bool rz = a.emul & 2, isplit = a.emul & 4;
-          for (int k = 0; k < K; ++k) {
-            float zh[4], zl[4];
-#pragma unroll
-            for (int y = 0; y < 4; ++y) {
-              float z = Bm[k * mp + c0 + y];
-              if (phase == 1 && isplit && k == c0 + y) z -= 1.f;
-              zh[y] = emu_rn_tf32(z);
-              zl[y] = emu_rn_tf32(z - zh[y]);
-            }
-#pragma unroll
-            for (int x = 0; x < RT; ++x) {
-              const float u = src[x * RS * ld + k];
-              const float uh = emu_rn_tf32(u), ul = emu_tr_tf32(u - uh);
-#pragma unroll
-              for (int y = 0; y < 4; ++y) {
-                if (a.emul & 8) {  // small terms first
-                  if (rz) {
-                    acc[x][y] = __fmaf_rz(ul, zh[y], acc[x][y]);
-                    acc[x][y] = __fmaf_rz(uh, zl[y], acc[x][y]);
-                    acc[x][y] = __fmaf_rz(uh, zh[y], acc[x][y]);
-                  } else {
-                    acc[x][y] = fmaf(ul, zh[y], acc[x][y]);
-                    acc[x][y] = fmaf(uh, zl[y], acc[x][y]);
-                    acc[x][y] = fmaf(uh, zh[y], acc[x][y]);
-                  }
-                } else if (rz) {
-                  acc[x][y] = __fmaf_rz(uh, zh[y], acc[x][y]);
-                  acc[x][y] = __fmaf_rz(uh, zl[y], acc[x][y]);
-                  acc[x][y] = __fmaf_rz(ul, zh[y], acc[x][y]);
-                } else {
-                  acc[x][y] = fmaf(uh, zh[y], acc[x][y]);
-                  acc[x][y] = fmaf(uh, zl[y], acc[x][y]);
-                  acc[x][y] = fmaf(ul, zh[y], acc[x][y]);
-                }
-              }
-            }
-          }
-          if (phase == 1 && isplit) {
-#pragma unroll
-            for (int x = 0; x < RT; ++x)
-#pragma unroll
-              for (int y = 0; y < 4; ++y) acc[x][y] += src[x * RS * ld + c0 + y];
-          }
-         } else {
 #pragma unroll 3
           for (int k = 0; k < K; k += 4) {
             float4 b[4];
@@ -456,7 +398,6 @@ __global__ void __launch_bounds__(kFThreads, 1)
               }
             }
           }
-         }
         } else {
           for (int k = 0; k < K; ++k) {
             T mz[4];

@@ -1745,7 +1745,6 @@ struct Lobpcg {
     ua.skip = status.p + 5;
     ua.wc = Wc.p;
     ua.part = colpart.p;
-    ua.emul = (int)env_double("MG_UPD_EMUL", 0);
     int nblk_upd = grid_upd;
     {
       ProfScope ps(ctx, PROF_UPDATE, 2.0 * n * ld * sizeof(T) + 5.0 * n * mp * sizeof(T));
@@ -1797,7 +1796,7 @@ struct Lobpcg {
                   nd);
           goto upd_done;
         }
-        if (upd_tc && !safe_mode && !ua.emul && update_tc3_supported(w, mp, ld) && w > upd_tc) {
+        if (upd_tc && !safe_mode && update_tc3_supported(w, mp, ld) && w > upd_tc) {
           tc_update_used = true;
           prev_update_tc = true;
           nblk_upd = update_tc3(ctx, n, ld, w, m, mp, (float *)S.p, (float *)AS.p,
@@ -1805,7 +1804,7 @@ struct Lobpcg {
                                 theta.p, status.p + 5, colpart.p, (float *)Wc.p);
           goto upd_done;
         }
-        if (upd_ws && !ua.emul) {
+        if (upd_ws) {
           UpdArgs uw = ua;
           uw.tk = tk_ws;
           prev_update_tc = false;
@@ -1970,11 +1969,7 @@ struct Lobpcg {
         double qn = std::sqrt(cr[mp + c]);
         cv[c] = rn[c] <= accept * tol * ((anorm + std::fabs(th[c]) * bmax) * qn) ? 1 : 0;
       }
-      // experiment (MG_CONV_COLS): only the first columns have to converge; the
-      // rest of the block rides along as guard vectors
-      static const int conv_cols = (int)env_double("MG_CONV_COLS", 0);
-      const int need = sizeof(T) == 4 && conv_cols > 0 && conv_cols < m ? conv_cols : m;
-      return std::all_of(cv.begin(), cv.begin() + need, [](int v) { return v != 0; });
+      return std::all_of(cv.begin(), cv.end(), [](int v) { return v != 0; });
     };
     std::vector<double> rn;
     std::vector<int> cv;
