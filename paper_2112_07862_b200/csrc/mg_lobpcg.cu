@@ -1469,6 +1469,7 @@ struct Lobpcg {
 
   // residual pass + one D2H of [rn^2 | qn^2 | theta | status]
   void iterate_sync(bool write_w, std::vector<double> &cr, std::vector<double> &th, int st[4]) {
+    if (write_w) w_layout_identity();  // k_resid writes W in natural order
     int R = std::max(1, 256 / mp);
     int bs = R * mp;
     int nb = grid_for(n, R, ctx->num_sms * 4);
@@ -1510,6 +1511,20 @@ struct Lobpcg {
   bool tc_update_used = false;  // some update of this solve ran on the tensor cores
   bool gram_prev_valid = false, refreshed_now = false, prev_update_tc = false;
   bool gram_narrow_now = false, safe_mode = false;
+  // Layout of the W block as last written.  wperm[c]: physical column (within
+  // the W region of S / AS) of logical column c.  The compact SpMM input Wc
+  // holds physical columns [wc0, wc0 + wcs) with row stride wcs.  Identity /
+  // (0, mp) unless the tensor-core update packed the unconverged columns into
+  // a suffix (MG_PACK_W): their gathered rows are then 128-byte lines.
+  std::vector<int> wperm, cv_now, next_perm;
+  int wc0 = 0, wcs = 0, next_wc0 = 0, next_wcs = 0;
+  bool next_identity = true;
+  void w_layout_identity() {
+    wperm.resize(mp);
+    std::iota(wperm.begin(), wperm.end(), 0);
+    wc0 = 0;
+    wcs = mp;
+  }
   // fp32 breakdown recovery: two alternating copies of X, taken every 8 healthy
   // iterations; restored (the older one) when the residuals blow up
   DBuf<T> ckpt[2];
@@ -1772,7 +1787,8 @@ struct Lobpcg {
           MG_CHECK_LAUNCH(ctx);
           nblk_upd = update_tc3(ctx, n, ld, w, m, mp, (float *)S.p, (float *)AS.p,
                                 (const float *)bw.p, (const float *)pr, (const float *)M.p,
-                                theta.p, status.p + 5, colpart.p, (float *)Wc.p);
+                                theta.p, status.p + 5, colpart.p, (float *)Wc.p, nullptr, 0, mp);
+          next_identity = true;
           k_upd_cmp<<<4 * ctx->num_sms, 256, 0, ctx->stream>>>((const float *)S.p, S2.p, n, ld, mp, 3, out.p);
           k_upd_cmp<<<4 * ctx->num_sms, 256, 0, ctx->stream>>>((const float *)AS.p, A2.p, n, ld, mp, 2, out.p + 8);
           k_upd_cmp<<<4 * ctx->num_sms, 256, 0, ctx->stream>>>((const float *)Wc.p, W2.p, n, mp, mp, 1, out.p + 16);
@@ -1799,15 +1815,42 @@ struct Lobpcg {
         if (upd_tc && !safe_mode && update_tc3_supported(w, mp, ld) && w > upd_tc) {
           tc_update_used = true;
           prev_update_tc = true;
+          // Pack the columns that are still unconverged into a suffix of the W
+          // block: the next SpMM then gathers rows of <= 32 columns at a 128-byte
+          // stride (one L1 line per gathered row instead of two) as soon as one
+          // column is locked, and its width follows the number of active columns
+          // instead of the length of the converged prefix.
+          const bool pack = env_double("MG_PACK_W", 1) != 0 && !comm && !have_y &&
+                            (int)cv_now.size() == m && !upd_tc_check;
+          if (pack) {
+            next_perm.assign(mp, 0);
+            int pos = 0, na = 0;
+            for (int c = 0; c < mp; ++c)
+              if (c >= m || cv_now[c]) next_perm[c] = pos++;
+            for (int c = 0; c < m; ++c)
+              if (!cv_now[c]) {
+                next_perm[c] = pos++;
+                ++na;
+              }
+            const int c0n = (mp - na) / VN * VN, wn = mp - c0n;
+            next_wcs = wn <= 32 ? 32 : mp;
+            next_wc0 = next_wcs == mp ? 0 : c0n;
+            next_identity = false;
+          } else {
+            next_identity = true;
+          }
           nblk_upd = update_tc3(ctx, n, ld, w, m, mp, (float *)S.p, (float *)AS.p,
                                 (const float *)bw.p, (const float *)pr, (const float *)M.p,
-                                theta.p, status.p + 5, colpart.p, (float *)Wc.p);
+                                theta.p, status.p + 5, colpart.p, (float *)Wc.p,
+                                next_identity ? nullptr : next_perm.data(),
+                                next_identity ? 0 : next_wc0, next_identity ? mp : next_wcs);
           goto upd_done;
         }
         if (upd_ws) {
           UpdArgs uw = ua;
           uw.tk = tk_ws;
           prev_update_tc = false;
+          next_identity = true;
           k_update_ws<4><<<grid_upd, kWsF + kWsS, ws_smem, ctx->stream>>>(
               (float *)S.p, (float *)AS.p, (const float *)bw.p, (const float *)pr,
               (const float *)M.p, theta.p, uw);
@@ -1815,6 +1858,7 @@ struct Lobpcg {
           goto upd_done;
         }
       }
+      next_identity = true;
       if (rt_upd == 8)
         k_update_resid<T, 3, 8><<<grid_upd, kFThreads, upd_smem, ctx->stream>>>(S.p, AS.p, bw.p,
                                                                                pr, M.p, theta.p, ua);
@@ -1875,6 +1919,14 @@ struct Lobpcg {
     if (st6[5]) {
       ++fast_fallbacks;
       return false;
+    }
+    // the update ran: W now has the layout it was given
+    if (next_identity) {
+      w_layout_identity();
+    } else {
+      wperm = next_perm;
+      wc0 = next_wc0;
+      wcs = next_wcs;
     }
     cr.assign(buf.begin(), buf.begin() + 2 * mp);
     th.assign(buf.begin() + 2 * mp, buf.begin() + 3 * mp);
@@ -2072,9 +2124,11 @@ struct Lobpcg {
         iterate_sync(true, cr, th, st);
         if (conv_test(rn, cv)) break;
       }
+      if ((int)wperm.size() != mp) w_layout_identity();
+      cv_now = cv;
       std::vector<int> vcols;
       for (int c = 0; c < m; ++c)
-        if (!cv[c]) vcols.push_back(2 * mp + c);
+        if (!cv[c]) vcols.push_back(2 * mp + wperm[c]);
       if (have_y) {
         deflate_cols(2 * mp, 3 * mp, 2 * mp, mp);
         k_copy_cols<T><<<grid_for(n * mp, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
@@ -2092,13 +2146,19 @@ struct Lobpcg {
         // the basis; they usually form a suffix (the smallest pairs converge
         // first), so A W is formed for the 16-byte-aligned column range that
         // covers them -- the images of locked columns are never read
-        int c0 = m;
+        int c0 = m;  // first physical W column that is active
         for (int c = 0; c < m; ++c)
-          if (!cv[c]) {
-            c0 = c;
-            break;
-          }
+          if (!cv[c]) c0 = std::min(c0, wperm[c]);
         c0 = c0 / VN * VN;
+        if (c0 < wc0) {
+          // a locked column became active again and lies outside the packed
+          // block: rebuild the compact copy of the whole W region
+          k_copy_cols<T><<<grid_for(n * mp, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+              n, S.p, ld, 2 * mp, Wc.p, mp, 0, mp);
+          MG_CHECK_LAUNCH(ctx);
+          wc0 = 0;
+          wcs = mp;
+        }
         {
           static const bool dbg_c0 = env_double("MG_DEBUG_C0", 0) != 0;
           if (dbg_c0) {
@@ -2110,7 +2170,7 @@ struct Lobpcg {
         if (comm)
           halo_spmm(Wc.p, mp, c0, mp - c0, AS.p + 2 * mp + c0, ld);
         else
-          spmm<T>(ctx, A, Wc.p + c0, mp, AS.p + 2 * mp + c0, ld, mp - c0);
+          spmm<T>(ctx, A, Wc.p + (c0 - wc0), wcs, AS.p + 2 * mp + c0, ld, mp - c0);
         debug_check("spmm");
       }
       for (int c = 0; c < pcount; ++c) vcols.push_back(mp + c);

@@ -32,7 +32,7 @@ void gram_w_tc2(mg_ctx *ctx, int64_t n, int ld, int w, int mp, const float *S, c
 bool update_tc3_supported(int w, int mp, int ld);
 int update_tc3(mg_ctx *ctx, int64_t n, int ld, int w, int m, int mp, float *S, float *AS,
                const float *b, const float *prec, const float *Mg, const double *theta,
-               const int *skip, double *part, float *wc);
+               const int *skip, double *part, float *wc, const int *perm, int wc0, int wcs);
 void update_f32_hook(mg_ctx *ctx, int variant, int64_t n, int ld, int m, int mp, float *S,
                      float *AS, const float *b, const float *prec, const float *Mg,
                      const double *theta, float *wc, double *colsums);

@@ -146,7 +146,11 @@ struct Upd3Args {
   int m;
   const int *skip;   // device flag: nonzero -> return (fallback iteration)
   double *part;      // [grid][2*mp] column partials (sum r^2, sum x^2)
-  float *wc;         // compact W (n x mp), the SpMM input
+  float *wc;         // compact W, the SpMM input: n x wcs, columns = physical W columns
+                     // [wc0, wc0 + wcs) (wcs = mp, wc0 = 0: the whole block)
+  int wcs, wc0;
+  int perm[40];      // physical W column of logical column c (identity unless the solver
+                     // packs the unconverged columns into a suffix)
   int dbg;           // MG_U3_DBG timing experiments: 1 no MMA, 2 no split, 4 no epilogue I/O
 };
 
@@ -213,6 +217,8 @@ __global__ void __launch_bounds__(kU3Threads, 1)
   const int64_t t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
   const int T = (int)(t_end - t_begin);
 
+  // compact-W slots beyond the block's last column are never written: keep them zero
+  for (int e = tid; e < (int)(3 * u3_obytes(MP) / 4); e += kU3Threads) obuf[e] = 0.f;
   if (tid == 0) {
     for (int s = 0; s < kU3NR; ++s) {
       mbar_init(&full[s], 1);
@@ -460,6 +466,7 @@ __global__ void __launch_bounds__(kU3Threads, 1)
         // 9.4 at C5).  Rows beyond n are clipped by the tensor maps.
         float *oS = obuf + (size_t)half * (16 * 6 * MP);
         float *oA = oS + 16 * W, *oW = oA + 16 * 2 * MP;
+        const int wcs = a.wcs;
         if (q == 0 && lane == 0)  // the previous chunk's stores have read the slot
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         asm volatile("bar.sync %0, %1;" ::"r"(2 + half), "n"(32 * NQ) : "memory");
@@ -473,6 +480,8 @@ __global__ void __launch_bounds__(kU3Threads, 1)
         const int64_t rr = row_of(u);
         const int nrow = (a.dbg & 8) ? 0 : (int)max((int64_t)0, min((int64_t)16, a.n - rr));
         if (isx) {
+          const int pc = a.perm[c];  // W's physical column, and its slot in the compact block
+          const int pcw = (pc >= a.wc0 && pc - a.wc0 < wcs) ? pc - a.wc0 : -1;
           float s1 = 0.f, s2 = 0.f;  // fp32 over the chunk's 16 rows, fp64 across chunks
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
@@ -489,8 +498,8 @@ __global__ void __launch_bounds__(kU3Threads, 1)
             }
             oS[e * W + c] = x1;
             oA[e * 2 * MP + c] = a1;
-            oS[e * W + 2 * MP + c] = wv;
-            oW[e * MP + c] = wv;
+            oS[e * W + 2 * MP + pc] = wv;
+            if (pcw >= 0) oW[e * wcs + pcw] = wv;
           }
           sr += (double)s1;
           sx += (double)s2;
@@ -618,7 +627,7 @@ static void launch_tc3(mg_ctx *ctx, int grid, const CUtensorMap &mS, const CUten
 // one fast-path update on the tensor cores; part: [grid][2 mp]; returns the grid
 int update_tc3(mg_ctx *ctx, int64_t n, int ld, int w, int m, int mp, float *S, float *AS,
                const float *b, const float *prec, const float *Mg, const double *theta,
-               const int *skip, double *part, float *wc) {
+               const int *skip, double *part, float *wc, const int *perm, int wc0, int wcs) {
   require(update_tc3_supported(w, mp, ld), MG_ERR_INTERNAL, "tc update: unsupported shape");
   require(((uintptr_t)S % 16) == 0 && ((uintptr_t)AS % 16) == 0, MG_ERR_INTERNAL,
           "tc update: operands must be 16-byte aligned");
@@ -628,6 +637,11 @@ int update_tc3(mg_ctx *ctx, int64_t n, int ld, int w, int m, int mp, float *S, f
   a.skip = skip;
   a.part = part;
   a.wc = wc;
+  require(wcs >= 4 && wcs <= mp && wcs % 4 == 0 && wc0 >= 0 && wc0 + wcs <= mp + 32, MG_ERR_INTERNAL,
+          "tc update: bad compact W layout");
+  a.wcs = wcs;
+  a.wc0 = wc0;
+  for (int c = 0; c < 40; ++c) a.perm[c] = (perm && c < mp) ? perm[c] : c;
   {
     const char *e = getenv("MG_U3_DBG");
     a.dbg = e ? atoi(e) : 0;
@@ -642,7 +656,7 @@ int update_tc3(mg_ctx *ctx, int64_t n, int ld, int w, int m, int mp, float *S, f
   // outputs: [X P W] of S, [AX AP] of AS, compact W (16-row boxes of complete rows)
   const CUtensorMap mOS = make_map_x(S, n, ld, 3 * mp, 3 * mp);
   const CUtensorMap mOA = make_map_x(AS, n, ld, 2 * mp, 2 * mp);
-  const CUtensorMap mOW = make_map_x(wc, n, mp, mp, mp);
+  const CUtensorMap mOW = make_map_x(wc, n, wcs, wcs, wcs);
   if (mp == 12)
     launch_tc3<12>(ctx, grid, mS, mA, mXS, mXA, mOS, mOA, mOW, S, AS, b, prec, Mg, theta, a);
   else if (mp == 20)
@@ -675,7 +689,8 @@ void update_f32_hook(mg_ctx *ctx, int variant, int64_t n, int ld, int m, int mp,
   DBuf<double> part(ctx, (size_t)ctx->num_sms * 2 * mp);
   int nb;
   if (variant == 1) {
-    nb = update_tc3(ctx, n, ld, w, m, mp, S, AS, b, prec, Mg, theta, skip.p, part.p, wc);
+    nb = update_tc3(ctx, n, ld, w, m, mp, S, AS, b, prec, Mg, theta, skip.p, part.p, wc, nullptr, 0,
+                    mp);
   } else {
     int tk = 0;
     for (int t = 256; t >= 32; t -= 4)
