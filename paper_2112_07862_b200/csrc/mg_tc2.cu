@@ -17,7 +17,7 @@
 //     sums such as diag(G_B) drift by ~2^-22 relative);
 //   * 2 MMAs per k-step: A_hi x [B_hi | B_lo] (hi*hi and hi*lo side by side,
 //     N = 64 pw) and A_lo x B_hi into the cross columns;
-//   * short TMEM accumulations (64 rows, double-buffered) drained into fp32
+//   * short TMEM accumulations (128 rows, double-buffered) drained into fp32
 //     registers, folded into fp64 every 2048 rows (the TC's fp32 adds are not
 //     round-to-nearest: 2048-row TMEM sums failed the 2e-6 bar).
 // Measured (profiles/r1_gram_tc.md): 11-13 ms at 20M x 108 vs 16.8 ms (v1);
@@ -40,8 +40,8 @@ constexpr int kG2Threads = 320;   // warp 0 TMA producer, warp 1 MMA issuer, 8 w
 constexpr int kG2TK = 32;         // rows per stage (4 MMA k-steps)
 constexpr int kG2Stages = 3;
 constexpr int kG2Panel = kG2TK * 128;  // bytes per 32-column panel of a stage
-constexpr int kG2FL = 2;          // tiles per TMEM accumulation group (64 rows)
-constexpr int kG2FoldG = 32;      // groups per fp64 fold (2048 rows)
+constexpr int kG2FL = 4;          // tiles per TMEM accumulation group (128 rows)
+constexpr int kG2FoldG = 16;      // groups per fp64 fold (2048 rows)
 
 __host__ __device__ constexpr size_t g2_smem_bytes(int pw) {
   return kG2Stages * ((size_t)4 * pw * kG2Panel + 128) + 256;
@@ -196,7 +196,7 @@ struct Gram2TcArgs {
 //   A_hi (TMA S, rounded in place) | A_lo | B_hi (bS, or TMA AS rounded in
 //   place) | B_lo
 // TMEM: 2 accumulation buffers x [hi*hi (32 pw columns) | cross (32 pw)]; a buffer
-// collects kG2FL tiles (64 rows) and is drained into fp32 registers while
+// collects kG2FL tiles (128 rows) and is drained into fp32 registers while
 // the other fills -- short tensor-core accumulations keep its fp32 adds'
 // rounding at the v1 level; registers fold into fp64 every kG2FoldG groups.
 __global__ void __launch_bounds__(kG2Threads, 1)

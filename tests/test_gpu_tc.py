@@ -1,6 +1,6 @@
 """tcgen05 (3xTF32) Gram pair vs an fp64 numpy Gram of the same fp32 data.
 
-3xTF32 products carry ~2^-21 relative error and the MMA accumulates 64 rows
+3xTF32 products carry ~2^-21 relative error and the MMA accumulates 128 rows
 in fp32 before the fp64-accurate fold, so the bar is 2e-6 of the Gram's scale
 (sum of |products|), tighter than the fp32 data's own 6e-8 per element times
 sqrt(rows) growth would allow for plain fp32 summation.
