@@ -61,7 +61,8 @@ def main():
         res, b, dg = core.embed_arrays(n, None, None, None, K, scfg, device_inputs=dev)
         torch.cuda.synchronize()
         print(f"rep {r}: {time.perf_counter() - t0:.3f} s, iterations {res.iterations}, "
-              f"eps_it {dg.eps_iterations}, ev[:4] {np.asarray(res.eigenvalues)[:4]}", flush=True)
+              f"eps_it {dg.eps_iterations}, ev[:4] {np.asarray(res.eigenvalues)[:4]}, "
+              f"setup {dg.seconds_setup:.3f} eps {dg.seconds_eps:.3f} solve {dg.seconds_solve:.3f}", flush=True)
     if args.stats:
         st = N.stats(0)
         N.set_profiling(False, 0)
