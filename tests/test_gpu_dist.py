@@ -108,3 +108,24 @@ def test_nccl_single_rank_communicator(mg):
     np.testing.assert_array_equal(e1.eigenvalues, e0.eigenvalues)
     np.testing.assert_array_equal(e1.P, e0.P)
     comm.close()
+
+
+def test_dist_c5_block_width_fast_paths(mg):
+    """K = 32 (w = 108), fp32: the tensor-core update, the narrow Gram with derived blocks
+    and the breakdown guard run under the row partition too (2 virtual ranks); every rank
+    ends with the same converged block, Ritz values equal to the single-GPU solve's to the
+    stopping rule's resolution."""
+    from paper_2112_07862_b200 import synthetic
+    g = synthetic.config_graph("c5", n=60_000)
+    cfg = mg.SolverConfig(k=33, tol=1e-4, max_iter=3000, seed=42, precision="fp32")
+    res0, b0, _ = _single(g, 32, cfg)
+    outs = _dist(g, 32, cfg, 2)
+    for res, b, dg in outs:
+        assert res.converged.all()
+        rel = np.abs(res.eigenvalues - res0.eigenvalues) / np.abs(res0.eigenvalues)
+        assert rel[:26].max() < 3e-3, rel
+        vecs = res.eigenvectors
+        gram = vecs.T @ (b[:, None] * vecs)
+        assert np.max(np.abs(gram - np.eye(33))) < 1e-4
+    np.testing.assert_array_equal(outs[0][0].eigenvalues, outs[1][0].eigenvalues)
+    np.testing.assert_array_equal(outs[0][0].eigenvectors, outs[1][0].eigenvectors)
