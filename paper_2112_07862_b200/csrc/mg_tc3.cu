@@ -387,8 +387,9 @@ __global__ void __launch_bounds__(kU3Threads, 1)
               const float4 h = make_float4(rn_tf32(x[i].x), rn_tf32(x[i].y), rn_tf32(x[i].z),
                                            rn_tf32(x[i].w));
               src[e] = h;
-              dst[e] = make_float4(rn_tf32(x[i].x - h.x), rn_tf32(x[i].y - h.y),
-                                   rn_tf32(x[i].z - h.z), rn_tf32(x[i].w - h.w));
+              // lo = x - hi is exact in fp32; the tensor core reads its top 11 bits
+              // (|lo| <= 2^-12 |x|: what it drops is below 2^-23 |x|, of either sign)
+              dst[e] = make_float4(x[i].x - h.x, x[i].y - h.y, x[i].z - h.z, x[i].w - h.w);
             }
           }
           fence_proxy_async();
