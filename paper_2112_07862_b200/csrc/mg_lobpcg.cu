@@ -62,7 +62,7 @@ __global__ void k_gram_derive1(const double *__restrict__ G0, const double *__re
 }
 __global__ void k_gram_derive2(const double *__restrict__ U, const float *__restrict__ Mg, int w,
                                int mp, int tc, double *__restrict__ G0, double *__restrict__ G1,
-                               double *__restrict__ dbg) {
+                               double *__restrict__ dbg, int check_only) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x, g = blockIdx.y;
   if (e >= 4 * mp * mp) return;
   const int a = e / (2 * mp), b = e - a * 2 * mp;
@@ -76,7 +76,7 @@ __global__ void k_gram_derive2(const double *__restrict__ U, const float *__rest
     atomicMax(reinterpret_cast<unsigned long long *>(dbg + 2 * g + 1),
               (unsigned long long)__double_as_longlong(fabs(G[a * w + b])));
   }
-  G[a * w + b] = s;
+  if (!check_only) G[a * w + b] = s;
 }
 
 // debug: largest |a - b| relative to the entries' diagonal scale sqrt(|b_ii b_jj|),
@@ -1703,7 +1703,7 @@ struct Lobpcg {
                                                   prev_update_tc ? 1 : 0, Uder.p);
       MG_CHECK_LAUNCH(ctx);
       k_gram_derive2<<<g2, 128, 0, ctx->stream>>>(Uder.p, (const float *)M.p, w, mp,
-                                                  prev_update_tc ? 1 : 0, Gr0.p, Gr1.p, nullptr);
+                                                  prev_update_tc ? 1 : 0, Gr0.p, Gr1.p, nullptr, 0);
       MG_CHECK_LAUNCH(ctx);
       if (gram_derive_mode & 2) {  // debug: against the full Gram pair of the same block
         DBuf<double> F0(ctx, (size_t)w * w), F1(ctx, (size_t)w * w), dd(ctx, 4);
@@ -1717,6 +1717,30 @@ struct Lobpcg {
         if ((iter_now % 20) == 3 || h[0] > 1e-4 || h[1] > 1e-4 || h[2] > 1e-4 || h[3] > 1e-4)
           fprintf(stderr, "[gram narrow it=%d] rel diff vs full: GB xp %.2e w %.2e | GA xp %.2e w %.2e\n",
                   iter_now, h[0], h[1], h[2], h[3]);
+      }
+    }
+    if (gram_derive_mode && sizeof(T) == 4 && !gram_narrow_now && gram_prev_valid && refreshed_now &&
+        gram_w_tc2_supported(w, mp, ld)) {
+      // Self-check at every A-image refresh, where the full pair was just reduced:
+      // the B-Gram blocks derived over the last cycle against the reduced ones (the
+      // A-Gram is not comparable here, its images were replaced).  A drift beyond
+      // 1e-3 of the blocks' scale switches the derived blocks off for this solve.
+      double *dbg = Uder.p + (size_t)2 * w * 2 * mp;
+      MG_CUDA(cudaMemsetAsync(dbg, 0, 4 * sizeof(double), ctx->stream));
+      dim3 g1((w * 2 * mp + 127) / 128, 2), g2((4 * mp * mp + 127) / 128, 2);
+      k_gram_derive1<<<g1, 128, 0, ctx->stream>>>(GBp.p, GAp.p, (const float *)M.p, w, mp,
+                                                  prev_update_tc ? 1 : 0, Uder.p);
+      MG_CHECK_LAUNCH(ctx);
+      k_gram_derive2<<<g2, 128, 0, ctx->stream>>>(Uder.p, (const float *)M.p, w, mp,
+                                                  prev_update_tc ? 1 : 0, Gr0.p, Gr1.p, dbg, 1);
+      MG_CHECK_LAUNCH(ctx);
+      double h[4];
+      d2h_sync(ctx, h, dbg, sizeof(h));
+      if (!(h[0] <= 1e-3 * h[1])) {
+        if (env_double("MG_DEBUG_RECOVER", 0) != 0)
+          fprintf(stderr, "[derive] it=%d: derived B-Gram blocks drifted %.2e of %.2e: full Gram pair from here on\n",
+                  iter_now, h[0], h[1]);
+        gram_derive_mode = 0;
       }
     }
     if (gram_derive_mode && sizeof(T) == 4) {
